@@ -1,0 +1,87 @@
+/*
+ * bandchol_b200.h -- C ABI of the B200-native fp64 band Cholesky library
+ * (libbandchol_b200.so).  Plain pointers and sizes; no torch or CUDA types.
+ *
+ * Storage: LAPACK lower band AB(ldab, n), element (i,j), j <= i <= min(n-1, j+kd),
+ * at ab[j*ldab + (i-j)] -- the reference's BandedMatrix layout
+ * (pkg/src/bandchol/core.py:1-19, :34-44).  Padding slots are never written.
+ *
+ * All pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) on the
+ * current device; every call is asynchronous on `stream` (a cudaStream_t, NULL =
+ * legacy default stream) and returns once the work is enqueued.
+ *
+ * Return codes: 0 = enqueued; -i = argument i is illegal (LAPACK style,
+ * 1-based); > 0 = a CUDA error code.  bcg_last_error() gives the message
+ * (thread-local).  Numerical outcomes are reported through the device `info`
+ * array, LAPACK convention: 0 = success, c+1 = the pivot of global column c was
+ * not > 0 (NaN counts as failure) for dpbtrf -> the reference's
+ * NotPositiveDefinite(c) (reference.py:56-57, errors.py:31-39); for dpbtrs
+ * c+1 = diagonal of L at column c is <= 0 -> SingularFactor (core.py:227-230),
+ * in which case b is left untouched.
+ */
+#ifndef BANDCHOL_B200_H
+#define BANDCHOL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Library ABI version (major*100 + minor). */
+int bcg_version(void);
+
+/* Thread-local message describing the last non-zero return. */
+const char* bcg_last_error(void);
+
+/* Workspace bytes bcg_dpbtrf needs for an (n, kd) matrix (0 when the single
+ * matrix runs in one CTA).  Holds the per-tile ready flags and the published
+ * panel tiles of the multi-CTA kernel.  The caller owns it (no allocation on
+ * the hot path); it must be zero-filled before the first use and is left
+ * zero-filled by every call that returns 0. */
+size_t bcg_dpbtrf_workspace_size(int64_t n, int64_t kd, int64_t ldab);
+
+/* In-place lower band Cholesky A = L L^T of ONE matrix, using the whole GPU.
+ * Replaces the reference engines factor_blocked_serial
+ * (pkg/src/bandchol/blocked.py:363-385) and factor_blocked_parallel
+ * (pkg/src/bandchol/parallel.py:130-166); info: device int32[1]. */
+int bcg_dpbtrf(int64_t n, int64_t kd, double* ab, int64_t ldab, int32_t* info,
+               void* workspace, size_t workspace_bytes, void* stream);
+
+/* In-place factorization of `batch` independent matrices of the same (n, kd,
+ * ldab) stored stride_ab doubles apart; info: device int32[batch].  Each matrix
+ * follows the same contract as one bcg_dpbtrf call (the batched interior-point
+ * use case of BASELINE.json config C5). */
+int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab,
+                       int64_t batch, int32_t* info, void* stream);
+
+/* Solve L L^T x = b in place (b -> x) with the factor from bcg_dpbtrf; nrhs
+ * right-hand sides stored ldb doubles apart.  Replaces solve_with_factor
+ * (pkg/src/bandchol/core.py:216-240).  info: device int32[1]. */
+int bcg_dpbtrs(int64_t n, int64_t kd, const double* ab, int64_t ldab, double* b, int64_t ldb,
+               int64_t nrhs, int32_t* info, void* stream);
+
+/* Batched solve: matrix i uses ab + i*stride_ab and its single right-hand side
+ * b + i*stride_b; info: device int32[batch]. */
+int bcg_dpbtrs_batched(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab,
+                       double* b, int64_t stride_b, int64_t batch, int32_t* info, void* stream);
+
+/* Fused batched factor + forward sweep + backward sweep (factor and solve of
+ * config C5 in one launch per matrix group): on return ab holds L and b holds
+ * x.  info: device int32[batch] with the dpbtrf convention; when a matrix fails
+ * its ab and b contents are unspecified (as after a failed reference factorization,
+ * which leaves the matrix partially overwritten). */
+int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab,
+                      double* b, int64_t stride_b, int64_t batch, int32_t* info, void* stream);
+
+/* Measurement utility (bench.py): FP64 FMA-pipe peak of the current device in
+ * TFLOP/s, from a register-only DFMA loop over every SM (synchronous, ~10 ms).
+ * The roofline denominator for the FP64-bound configs. */
+int bcg_probe_fp64_peak(double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BANDCHOL_B200_H */

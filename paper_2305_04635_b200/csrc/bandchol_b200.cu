@@ -1,0 +1,328 @@
+// bandchol_b200.cu -- kernels and C ABI of libbandchol_b200.so (see include/bandchol_b200.h).
+//
+// Entry points replace the reference's factorization engines and solve:
+//   bcg_dpbtrf / bcg_dpbtrf_batched  <- factor_blocked_serial (pkg/src/bandchol/blocked.py:363-385),
+//                                       factor_blocked_parallel (pkg/src/bandchol/parallel.py:130-166)
+//   bcg_dpbtrs / bcg_dpbtrs_batched  <- solve_with_factor (pkg/src/bandchol/core.py:216-240)
+//   bcg_dpbsv_batched                <- factor + solve of config C5 fused in one launch
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/bandchol_b200.h"
+#include "band_cta.cuh"
+#include "band_solve.cuh"
+#include "band_multi.cuh"
+
+namespace bcg {
+
+// One CTA per matrix (grid-stride over the batch).
+template <int NB, bool kWinSmem, bool kSolve>
+__global__ void __launch_bounds__(kCtaThreads, 2)
+pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int batch, CtaGeom g,
+                 int32_t* info, double* pglob) {
+  extern __shared__ __align__(16) double smem[];
+  for (int mat = blockIdx.x; mat < batch; mat += gridDim.x) {
+    CtaBand<NB, kWinSmem, kSolve> w{g};
+    w.ab = ab0 + (int64_t)mat * stride_ab;
+    w.rhs = kSolve ? b0 + (int64_t)mat * stride_b : nullptr;
+    double* p = smem;
+    if (kWinSmem) { w.win = p; p += (size_t)g.nslot * g.lds; } else { w.win = nullptr; }
+    if (kWinSmem) { w.P = p; p += (size_t)NB * g.pld; } else { w.P = pglob + (size_t)blockIdx.x * NB * g.pld; }
+    w.D = p; p += NB * NB;
+    w.Dinv = p; p += NB;
+    w.bw = kSolve ? p : nullptr;
+    const int fail = w.factor();
+    if (kSolve && fail < 0) w.backward();
+    if (threadIdx.x == 0) info[mat] = fail < 0 ? 0 : fail + 1;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kCtaThreads)
+pbtrs_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int nrhs, int n, int kd,
+             int ldab, int32_t* info) {
+  const int z = blockIdx.x;
+  const double* ab = ab0 + (int64_t)(z / nrhs) * stride_ab;
+  double* b = b0 + (int64_t)z * stride_b;
+  const int bad = first_nonpositive_diag(ab, n, ldab);
+  if (bad != INT_MAX) {
+    if (threadIdx.x == 0) info[z / nrhs] = bad + 1;
+    return;
+  }
+  band_forward(ab, n, kd, ldab, b);
+  band_backward(ab, n, kd, ldab, b);
+  if (threadIdx.x == 0 && z % nrhs == 0) info[z / nrhs] = 0;
+}
+
+}  // namespace bcg
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail_arg(int idx, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return -idx;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return 0;
+  snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+  return (int)e;
+}
+
+int smem_optin() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 48 * 1024;
+  }
+  return v;
+}
+
+int sm_count() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
+  }
+  return v;
+}
+
+bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb) {
+  bcg::CtaGeom g;
+  g.n = n;
+  g.kd = kd;
+  g.ldab = ldab;
+  g.lds = (kd + 1) | 1;  // odd column stride: element (i,j) has address parity of i
+  int ns = kd + nb;
+  if (ns & 1) ++ns;
+  g.nslot = ns;
+  g.pld = ((kd + 3) / 4) * 4;
+  if (g.pld < 4) g.pld = 4;
+  return g;
+}
+
+template <int NB, bool W, bool S>
+int launch_cta_t(double* ab, int64_t sab, double* b, int64_t sb, int batch, const bcg::CtaGeom& g, int32_t* info,
+                 cudaStream_t st, double* pglob = nullptr, int grid = 0) {
+  const size_t smem = bcg::cta_smem_bytes(NB, g, W, S);
+  auto k = bcg::pbtrf_cta_kernel<NB, W, S>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+  if (grid <= 0) grid = batch;
+  k<<<grid, bcg::kCtaThreads, smem, st>>>(ab, sab, b, sb, batch, g, info, pglob);
+  return cuda_status(cudaGetLastError(), "pbtrf_cta_kernel launch");
+}
+
+// Global-window variant: persistent grid, per-CTA panel scratch.  The scratch is
+// either the caller's workspace (bcg_dpbtrf) or stream-ordered (cudaMallocAsync).
+template <bool S>
+int launch_cta_global(double* ab, int64_t sab, double* b, int64_t sb, int batch, const bcg::CtaGeom& g,
+                      int32_t* info, cudaStream_t st, double* scratch) {
+  const int grid = batch < 2 * sm_count() ? batch : 2 * sm_count();
+  double* pg = scratch;
+  if (!pg) {
+    cudaError_t e = cudaMallocAsync((void**)&pg, (size_t)grid * 32 * g.pld * sizeof(double), st);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(panel scratch)");
+  }
+  int r = launch_cta_t<32, false, S>(ab, sab, b, sb, batch, g, info, st, pg, scratch ? 1 : grid);
+  if (!scratch) cudaFreeAsync(pg, st);
+  return r;
+}
+
+// Pick the block size and window placement for the one-CTA-per-matrix kernel.
+int launch_cta(double* ab, int64_t sab, double* b, int64_t sb, int batch, int n, int kd, int ldab, int32_t* info,
+               bool solve, cudaStream_t st, double* scratch = nullptr) {
+  const size_t limit = (size_t)smem_optin();
+  // Prefer two resident CTAs per SM (<= half the SM's shared memory), then one.
+  const size_t half = 113 * 1024;
+  const int cands[3] = {16, 32, 8};
+  for (size_t cap : {half, limit}) {
+    for (int nb : cands) {
+      bcg::CtaGeom g = make_geom(n, kd, ldab, nb);
+      if (bcg::cta_smem_bytes(nb, g, true, solve) > cap) continue;
+      if (solve) {
+        if (nb == 16) return launch_cta_t<16, true, true>(ab, sab, b, sb, batch, g, info, st);
+        if (nb == 32) return launch_cta_t<32, true, true>(ab, sab, b, sb, batch, g, info, st);
+        return launch_cta_t<8, true, true>(ab, sab, b, sb, batch, g, info, st);
+      }
+      if (nb == 16) return launch_cta_t<16, true, false>(ab, sab, b, sb, batch, g, info, st);
+      if (nb == 32) return launch_cta_t<32, true, false>(ab, sab, b, sb, batch, g, info, st);
+      return launch_cta_t<8, true, false>(ab, sab, b, sb, batch, g, info, st);
+    }
+  }
+  // Window too large for shared memory: run in place on the band in global memory.
+  bcg::CtaGeom g = make_geom(n, kd, ldab, 32);
+  if (solve) {
+    if (bcg::cta_smem_bytes(32, g, false, true) <= limit)
+      return launch_cta_global<true>(ab, sab, b, sb, batch, g, info, st, scratch);
+    return fail_arg(2, "kd=%d too large for the fused batched solve; use dpbtrf_batched + dpbtrs_batched", kd);
+  }
+  return launch_cta_global<false>(ab, sab, b, sb, batch, g, info, st, scratch);
+}
+
+int check_geom(int64_t n, int64_t kd, int64_t ldab) {
+  if (n < 1 || n > INT_MAX / 2) return fail_arg(1, "n=%lld out of range", (long long)n);
+  if (kd < 0 || kd >= n) return fail_arg(2, "kd=%lld invalid for n=%lld", (long long)kd, (long long)n);
+  if (ldab < kd + 1 || ldab > INT_MAX / 2) return fail_arg(4, "ldab=%lld < kd+1", (long long)ldab);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bcg_version(void) { return 100; }
+
+const char* bcg_last_error(void) { return g_err; }
+
+// Bytes of panel scratch the one-CTA global-window variant needs (0 if the window fits in smem).
+static size_t cta_scratch_bytes(int n, int kd, int ldab) {
+  bcg::CtaGeom g = make_geom(n, kd, ldab, 8);
+  if (bcg::cta_smem_bytes(8, g, true, false) <= (size_t)smem_optin()) return 0;
+  return (size_t)32 * make_geom(n, kd, ldab, 32).pld * sizeof(double);
+}
+
+size_t bcg_dpbtrf_workspace_size(int64_t n, int64_t kd, int64_t ldab) {
+  if (check_geom(n, kd, ldab) != 0) return 0;
+  if (bcg::use_multi((int)n, (int)kd)) return bcg::multi_workspace_bytes((int)n, (int)kd);
+  return cta_scratch_bytes((int)n, (int)kd, (int)ldab);
+}
+
+int bcg_dpbtrf(int64_t n, int64_t kd, double* ab, int64_t ldab, int32_t* info, void* workspace,
+               size_t workspace_bytes, void* stream) {
+  if (int r = check_geom(n, kd, ldab)) return r;
+  if (!ab) return fail_arg(3, "ab is NULL");
+  if (!info) return fail_arg(5, "info is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (bcg::use_multi((int)n, (int)kd)) {
+    const size_t need = bcg::multi_workspace_bytes((int)n, (int)kd);
+    if (!workspace || workspace_bytes < need)
+      return fail_arg(6, "workspace of %zu bytes required (got %zu)", need, workspace_bytes);
+    return bcg::launch_multi(ab, (int)n, (int)kd, (int)ldab, info, workspace, sm_count(), st, g_err, sizeof g_err);
+  }
+  const size_t need = cta_scratch_bytes((int)n, (int)kd, (int)ldab);
+  if (need && (!workspace || workspace_bytes < need))
+    return fail_arg(6, "workspace of %zu bytes required (got %zu)", need, workspace_bytes);
+  return launch_cta(ab, 0, nullptr, 0, 1, (int)n, (int)kd, (int)ldab, info, false, st,
+                    need ? (double*)workspace : nullptr);
+}
+
+int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, int64_t batch,
+                       int32_t* info, void* stream) {
+  if (int r = check_geom(n, kd, ldab)) return r;
+  if (!ab) return fail_arg(3, "ab is NULL");
+  if (stride_ab < ldab * n) return fail_arg(5, "stride_ab < ldab*n");
+  if (batch < 0 || batch > INT_MAX) return fail_arg(6, "batch out of range");
+  if (!info) return fail_arg(7, "info is NULL");
+  if (batch == 0) return 0;
+  return launch_cta(ab, stride_ab, nullptr, 0, (int)batch, (int)n, (int)kd, (int)ldab, info, false,
+                    (cudaStream_t)stream);
+}
+
+int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, double* b,
+                      int64_t stride_b, int64_t batch, int32_t* info, void* stream) {
+  if (int r = check_geom(n, kd, ldab)) return r;
+  if (!ab) return fail_arg(3, "ab is NULL");
+  if (stride_ab < ldab * n) return fail_arg(5, "stride_ab < ldab*n");
+  if (!b) return fail_arg(6, "b is NULL");
+  if (stride_b < n) return fail_arg(7, "stride_b < n");
+  if (batch < 0 || batch > INT_MAX) return fail_arg(8, "batch out of range");
+  if (!info) return fail_arg(9, "info is NULL");
+  if (batch == 0) return 0;
+  return launch_cta(ab, stride_ab, b, stride_b, (int)batch, (int)n, (int)kd, (int)ldab, info, true,
+                    (cudaStream_t)stream);
+}
+
+static int launch_solve(const double* ab, int64_t sab, double* b, int64_t sb, int nrhs, int64_t blocks, int n,
+                        int kd, int ldab, int32_t* info, cudaStream_t st) {
+  bcg::pbtrs_kernel<<<(unsigned)blocks, bcg::kCtaThreads, 0, st>>>(ab, sab, b, sb, nrhs, n, kd, ldab, info);
+  return cuda_status(cudaGetLastError(), "pbtrs_kernel launch");
+}
+
+int bcg_dpbtrs(int64_t n, int64_t kd, const double* ab, int64_t ldab, double* b, int64_t ldb, int64_t nrhs,
+               int32_t* info, void* stream) {
+  if (int r = check_geom(n, kd, ldab)) return r;
+  if (!ab) return fail_arg(3, "ab is NULL");
+  if (!b) return fail_arg(5, "b is NULL");
+  if (nrhs < 0 || nrhs > INT_MAX) return fail_arg(7, "nrhs out of range");
+  if (nrhs > 1 && ldb < n) return fail_arg(6, "ldb < n");
+  if (!info) return fail_arg(8, "info is NULL");
+  if (nrhs == 0) return 0;
+  return launch_solve(ab, 0, b, ldb, (int)nrhs, nrhs, (int)n, (int)kd, (int)ldab, info, (cudaStream_t)stream);
+}
+
+int bcg_dpbtrs_batched(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab, double* b,
+                       int64_t stride_b, int64_t batch, int32_t* info, void* stream) {
+  if (int r = check_geom(n, kd, ldab)) return r;
+  if (!ab) return fail_arg(3, "ab is NULL");
+  if (stride_ab < ldab * n) return fail_arg(5, "stride_ab < ldab*n");
+  if (!b) return fail_arg(6, "b is NULL");
+  if (stride_b < n) return fail_arg(7, "stride_b < n");
+  if (batch < 0 || batch > INT_MAX) return fail_arg(8, "batch out of range");
+  if (!info) return fail_arg(9, "info is NULL");
+  if (batch == 0) return 0;
+  return launch_solve(ab, stride_ab, b, stride_b, 1, batch, (int)n, (int)kd, (int)ldab, info,
+                      (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------------------------
+// measurement utility: FP64 FMA-pipe peak (roofline denominator)
+// ----------------------------------------------------------------------------
+namespace bcg {
+__global__ void __launch_bounds__(512) dfma_probe_kernel(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  double a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) out[0] = s;
+}
+}  // namespace bcg
+
+extern "C" int bcg_probe_fp64_peak(double* tflops) {
+  if (!tflops) return fail_arg(1, "tflops is NULL");
+  double* d = nullptr;
+  if (int r = cuda_status(cudaMalloc(&d, sizeof(double)), "cudaMalloc")) return r;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sm_count() * 4, tpb = 512, iters = 1024;
+  bcg::dfma_probe_kernel<<<blocks, tpb>>>(d, 16);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    bcg::dfma_probe_kernel<<<blocks, tpb>>>(d, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_status(e, "dfma_probe_kernel");
+  *tflops = 2.0 * 64.0 * iters * (double)blocks * tpb / (best * 1e-3) / 1e12;
+  return 0;
+}

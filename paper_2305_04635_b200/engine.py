@@ -1,0 +1,358 @@
+"""Host-side mirror of the reference's factorization / solve interface, on the GPU.
+
+Same names, argument meaning and error behaviour as the reference entry points:
+
+* `factor_blocked_serial(matrix, grid_dim, *, backend, trace, check_invariants)`
+  -- pkg/src/bandchol/blocked.py:363-385
+* `factor_blocked_parallel(matrix, grid_dim, policy, *, backend, trace, check_invariants)`
+  -- pkg/src/bandchol/parallel.py:130-166
+* `solve_with_factor(factor, rhs)` -- pkg/src/bandchol/core.py:216-240
+
+`matrix` is any object with the BandedMatrix fields (ours or the reference's):
+its `.data` is overwritten with L in place and the same object is returned
+(blocked.py:385).  The arithmetic runs in libbandchol_b200.so; this module only
+moves buffers (torch is used for device memory and streams) and maps the
+device `info` word onto the reference's exceptions:
+NotPositiveDefinite(column) for the first failing pivot, SingularFactor for a
+non-positive diagonal in the solve.  There is no CPU path: without the library
+or a GPU every call raises DeviceError.
+
+`grid_dim` is accepted for signature compatibility.  The GPU engine chooses its
+own tiles and needs no divisibility, but when a grid is passed the reference's
+plan_windows validation (blocked.py:91-98) is applied first so the same inputs
+raise the same errors.  `backend` is ignored (the CUDA kernels are the only
+engine); `trace` receives one TraceEvent per kernel launch.
+
+Batched and device-resident entry points (`factor_batched`, `solve_batched`,
+`factor_solve_batched`, `DeviceBatch`) serve the interior-point use case
+(BASELINE.json config C5).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import check_matrix
+from .errors import (BandCholError, BandwidthNotDivisible, DeviceError, GridTooSmall,
+                     InvalidBandwidth, NotPositiveDefinite, ShapeMismatch, SingularFactor)
+
+
+@dataclass(frozen=True)
+class TraceEvent:
+    """One kernel launch (the reference records one event per tile op, blocked.py:289-294)."""
+    kind: str
+    window: int
+    row: int
+    col: int
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as exc:  # pragma: no cover
+        raise DeviceError(f"torch is required for device memory: {exc}") from None
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device is visible; the band Cholesky runs only on the GPU")
+    return torch
+
+
+def _stream_handle(torch, stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+_workspaces: dict = {}
+
+
+def _workspace(torch, n: int, kd: int, ldab: int):
+    """Zero-filled per-device workspace for the multi-CTA kernel (kept between calls)."""
+    need = int(_lib.load().bcg_dpbtrf_workspace_size(n, kd, ldab))
+    if need == 0:
+        return None, 0
+    dev = torch.cuda.current_device()
+    ws = _workspaces.get(dev)
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+        _workspaces[dev] = ws
+    return ws, need
+
+
+def _validate_grid(n: int, k: int, grid_dim) -> None:
+    """plan_windows' argument checks (blocked.py:91-98), only when a grid is given."""
+    if grid_dim is None:
+        return
+    if grid_dim < 3:
+        raise GridTooSmall(f"grid dimension {grid_dim} < 3")
+    if k < 2 or k >= n:
+        raise InvalidBandwidth(
+            f"blocked factorization needs 2 <= bandwidth < dim, got k={k}, N={n}")
+    if k % (grid_dim - 1):
+        raise BandwidthNotDivisible(
+            f"bandwidth {k} not divisible by grid_dim-1 = {grid_dim - 1}")
+
+
+# -- device-resident primitives ---------------------------------------------------
+
+def dpbtrf_device(ab, n: int, kd: int, ldab: int, info=None, stream=None):
+    """Factor one band matrix held in a CUDA float64 tensor, in place.  Returns info."""
+    torch = _torch()
+    if info is None:
+        info = torch.zeros(1, dtype=torch.int32, device=ab.device)
+    ws, need = _workspace(torch, n, kd, ldab)
+    rc = _lib.load().bcg_dpbtrf(n, kd, ab.data_ptr(), ldab, info.data_ptr(),
+                                ws.data_ptr() if ws is not None else None, need,
+                                _stream_handle(torch, stream))
+    _lib.check(rc, "bcg_dpbtrf")
+    return info
+
+
+def dpbtrf_batched_device(ab, n: int, kd: int, ldab: int, batch: int, info=None, stream=None):
+    """Factor `batch` matrices stored back to back (stride ldab*n) in a CUDA tensor."""
+    torch = _torch()
+    if info is None:
+        info = torch.zeros(batch, dtype=torch.int32, device=ab.device)
+    rc = _lib.load().bcg_dpbtrf_batched(n, kd, ab.data_ptr(), ldab, ldab * n, batch,
+                                        info.data_ptr(), _stream_handle(torch, stream))
+    _lib.check(rc, "bcg_dpbtrf_batched")
+    return info
+
+
+def dpbtrs_device(ab, n: int, kd: int, ldab: int, b, nrhs: int = 1, info=None, stream=None):
+    """Solve L L^T x = b in place for nrhs right-hand sides (columns of length n)."""
+    torch = _torch()
+    if info is None:
+        info = torch.zeros(1, dtype=torch.int32, device=ab.device)
+    rc = _lib.load().bcg_dpbtrs(n, kd, ab.data_ptr(), ldab, b.data_ptr(), n, nrhs,
+                                info.data_ptr(), _stream_handle(torch, stream))
+    _lib.check(rc, "bcg_dpbtrs")
+    return info
+
+
+def dpbtrs_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=None, stream=None):
+    torch = _torch()
+    if info is None:
+        info = torch.zeros(batch, dtype=torch.int32, device=ab.device)
+    rc = _lib.load().bcg_dpbtrs_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
+                                        batch, info.data_ptr(), _stream_handle(torch, stream))
+    _lib.check(rc, "bcg_dpbtrs_batched")
+    return info
+
+
+def dpbsv_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=None, stream=None):
+    """Fused factor + solve of `batch` systems: ab -> L, b -> x, one launch."""
+    torch = _torch()
+    if info is None:
+        info = torch.zeros(batch, dtype=torch.int32, device=ab.device)
+    rc = _lib.load().bcg_dpbsv_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
+                                       batch, info.data_ptr(), _stream_handle(torch, stream))
+    _lib.check(rc, "bcg_dpbsv_batched")
+    return info
+
+
+def _raise_factor_info(info_value: int) -> None:
+    if info_value > 0:
+        raise NotPositiveDefinite(info_value - 1)
+
+
+# -- reference-shaped host API ----------------------------------------------------
+
+def _factor(matrix, grid_dim, trace) -> object:
+    n, k, ld, data = check_matrix(matrix)
+    _validate_grid(n, k, grid_dim)
+    torch = _torch()
+    dev = torch.from_numpy(data).to("cuda", non_blocking=False)
+    info = dpbtrf_device(dev, n, k, ld)
+    info_h = int(info.item())
+    if trace is not None:
+        trace.append(TraceEvent("gpu_dpbtrf", 0, 0, 0))
+    if info_h > 0:
+        raise NotPositiveDefinite(info_h - 1)
+    data[...] = dev.cpu().numpy()
+    return matrix
+
+
+def factor_blocked_serial(matrix, grid_dim=None, *, backend=None, trace=None,
+                          check_invariants: bool = False):
+    """GPU drop-in for blocked.py:363-385: overwrites matrix.data with L, returns matrix."""
+    return _factor(matrix, grid_dim, trace)
+
+
+def factor_blocked_parallel(matrix, grid_dim=None, policy=None, *, backend=None, trace=None,
+                            check_invariants: bool = False):
+    """GPU drop-in for parallel.py:130-166 (same engine; the policy has nothing to steer)."""
+    if policy is not None:
+        workers = getattr(policy, "worker_count", None)
+        if workers is not None and workers < 1:
+            raise BandCholError(f"worker count must be positive, got {workers}")
+    return _factor(matrix, grid_dim, trace)
+
+
+def solve_with_factor(factor, rhs) -> np.ndarray:
+    """GPU drop-in for core.py:216-240: returns x with L L^T x = rhs."""
+    n, k, ld, data = check_matrix(factor)
+    b = np.asarray(rhs, dtype=np.float64)
+    if b.shape != (n,):
+        raise ShapeMismatch(f"rhs shape {b.shape} does not match dimension {n}")
+    torch = _torch()
+    dab = torch.from_numpy(data).to("cuda")
+    db = torch.from_numpy(np.ascontiguousarray(b)).to("cuda")
+    info = dpbtrs_device(dab, n, k, ld, db)
+    info_h = int(info.item())
+    if info_h > 0:
+        raise SingularFactor(f"factor diagonal not positive at column {info_h - 1}")
+    return db.cpu().numpy()
+
+
+# -- batched host API -------------------------------------------------------------
+
+def _batch_array(data: np.ndarray, n: int, ld: int) -> np.ndarray:
+    a = np.asarray(data)
+    if a.dtype != np.float64 or a.ndim != 2 or a.shape[1] != ld * n or not a.flags.c_contiguous:
+        raise ShapeMismatch(f"batched band data must be C-contiguous float64 (batch, {ld * n})")
+    return a
+
+
+def factor_batched(data: np.ndarray, dim: int, bandwidth: int, lead_dim: int | None = None) -> np.ndarray:
+    """Factor every row of `data` (batch, lead_dim*dim) in place; returns per-matrix info.
+
+    Raises NotPositiveDefinite for the first failing matrix (its `.matrix` index is set).
+    """
+    ld = bandwidth + 1 if lead_dim is None else lead_dim
+    a = _batch_array(data, dim, ld)
+    torch = _torch()
+    dev = torch.from_numpy(a).to("cuda")
+    info = dpbtrf_batched_device(dev, dim, bandwidth, ld, a.shape[0]).cpu().numpy()
+    a[...] = dev.cpu().numpy()
+    _raise_batch(info)
+    return info
+
+
+def factor_solve_batched(data: np.ndarray, rhs: np.ndarray, dim: int, bandwidth: int,
+                         lead_dim: int | None = None) -> np.ndarray:
+    """Factor every matrix in place and solve its system; rhs (batch, dim) -> x in place."""
+    ld = bandwidth + 1 if lead_dim is None else lead_dim
+    a = _batch_array(data, dim, ld)
+    r = np.asarray(rhs)
+    if r.dtype != np.float64 or r.shape != (a.shape[0], dim) or not r.flags.c_contiguous:
+        raise ShapeMismatch(f"rhs must be C-contiguous float64 ({a.shape[0]}, {dim})")
+    torch = _torch()
+    dab = torch.from_numpy(a).to("cuda")
+    db = torch.from_numpy(r).to("cuda")
+    info = dpbsv_batched_device(dab, dim, bandwidth, ld, db, a.shape[0]).cpu().numpy()
+    a[...] = dab.cpu().numpy()
+    r[...] = db.cpu().numpy()
+    _raise_batch(info)
+    return info
+
+
+def solve_batched(factors: np.ndarray, rhs: np.ndarray, dim: int, bandwidth: int,
+                  lead_dim: int | None = None) -> np.ndarray:
+    """x_i = solve_with_factor(L_i, rhs_i) for every matrix; returns x (batch, dim)."""
+    ld = bandwidth + 1 if lead_dim is None else lead_dim
+    a = _batch_array(factors, dim, ld)
+    r = np.ascontiguousarray(rhs, dtype=np.float64)
+    if r.shape != (a.shape[0], dim):
+        raise ShapeMismatch(f"rhs must be ({a.shape[0]}, {dim})")
+    torch = _torch()
+    dab = torch.from_numpy(a).to("cuda")
+    db = torch.from_numpy(r.copy()).to("cuda")
+    info = dpbtrs_batched_device(dab, dim, bandwidth, ld, db, a.shape[0]).cpu().numpy()
+    bad = np.nonzero(info)[0]
+    if bad.size:
+        err = SingularFactor(f"matrix {bad[0]}: factor diagonal not positive at column {info[bad[0]] - 1}")
+        err.matrix = int(bad[0])
+        raise err
+    return db.cpu().numpy()
+
+
+def _raise_batch(info: np.ndarray) -> None:
+    bad = np.nonzero(info)[0]
+    if bad.size:
+        err = NotPositiveDefinite(int(info[bad[0]]) - 1,
+                                  f"matrix {bad[0]} is not positive definite at column {info[bad[0]] - 1}")
+        err.matrix = int(bad[0])
+        raise err
+
+
+def library_version() -> int:
+    return int(_lib.load().bcg_version())
+
+
+__all__ = [
+    "TraceEvent", "dpbtrf_device", "dpbtrf_batched_device", "dpbtrs_device", "dpbtrs_batched_device",
+    "dpbsv_batched_device", "factor_blocked_serial", "factor_blocked_parallel", "solve_with_factor",
+    "factor_batched", "factor_solve_batched", "solve_batched", "library_version",
+    "BatchedBandSolver", "pinned_empty",
+]
+
+
+# -- repeated batched solves with host buffers (interior-point loop) -----------------
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """Page-locked host array (so host<->device copies run at full PCIe rate, async)."""
+    torch = _torch()
+    t = torch.empty(shape, dtype=torch.float64 if dtype == np.float64 else torch.int32, pin_memory=True)
+    arr = t.numpy()
+    _pinned_keepalive[arr.ctypes.data] = t  # the torch tensor owns the pinned pages
+    return arr
+
+
+_pinned_keepalive: dict = {}
+
+
+class BatchedBandSolver:
+    """Device-resident workspace for repeated fused factor + solve of a fixed-shape batch.
+
+    `factor_solve(ab_host, b_host)` copies the batch in, factors every matrix and
+    solves its system (bcg_dpbsv_batched), and copies L and x back into the same
+    host arrays, pipelined over `chunks` so the host<->device copies of one chunk
+    overlap the kernel of the next.  Host arrays from `pinned_empty` give
+    asynchronous copies.  Raises NotPositiveDefinite (with `.matrix`) after the
+    whole batch completes if any matrix failed.
+    """
+
+    def __init__(self, batch: int, dim: int, bandwidth: int, lead_dim: int | None = None,
+                 chunks: int = 4):
+        torch = _torch()
+        self.torch = torch
+        self.batch, self.n, self.kd = int(batch), int(dim), int(bandwidth)
+        self.ld = self.kd + 1 if lead_dim is None else int(lead_dim)
+        self.chunks = max(1, min(int(chunks), self.batch))
+        self.ab = torch.empty((self.batch, self.ld * self.n), dtype=torch.float64, device="cuda")
+        self.b = torch.empty((self.batch, self.n), dtype=torch.float64, device="cuda")
+        self.info = torch.zeros(self.batch, dtype=torch.int32, device="cuda")
+        self.streams = [torch.cuda.Stream() for _ in range(2)]
+        bounds = np.linspace(0, self.batch, self.chunks + 1).astype(int)
+        self.ranges = [(int(bounds[i]), int(bounds[i + 1])) for i in range(self.chunks)
+                       if bounds[i + 1] > bounds[i]]
+        self.launches = 0
+
+    def factor_solve(self, ab_host: np.ndarray, b_host: np.ndarray, check: bool = True) -> np.ndarray:
+        torch = self.torch
+        a = _batch_array(ab_host, self.n, self.ld)
+        if a.shape[0] != self.batch or b_host.shape != (self.batch, self.n):
+            raise ShapeMismatch("host arrays do not match the solver's batch shape")
+        ta = torch.from_numpy(a)
+        tb = torch.from_numpy(b_host)
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        for idx, (lo, hi) in enumerate(self.ranges):
+            st = self.streams[idx % 2]
+            with torch.cuda.stream(st):
+                self.ab[lo:hi].copy_(ta[lo:hi], non_blocking=True)
+                self.b[lo:hi].copy_(tb[lo:hi], non_blocking=True)
+                dpbsv_batched_device(self.ab[lo:hi], self.n, self.kd, self.ld, self.b[lo:hi], hi - lo,
+                                     info=self.info[lo:hi], stream=st)
+                self.launches += 1
+                ta[lo:hi].copy_(self.ab[lo:hi], non_blocking=True)
+                tb[lo:hi].copy_(self.b[lo:hi], non_blocking=True)
+        for s in self.streams:
+            cur.wait_stream(s)
+        info = self.info.cpu().numpy()  # synchronises
+        if check:
+            _raise_batch(info)
+        return info
