@@ -145,7 +145,7 @@ struct CtaBand {
       if (c < nb) {
         const double yc = __shfl_sync(kFull, s, c) * Dinv[c];
         if (r == c) s = yc;
-        else if (r > c) s = fma(-D[r * NB + c], yc, s);
+        else if (r > c && r < nb) s = fma(-D[r * NB + c], yc, s);
       }
     }
     if (r < nb) {
@@ -238,6 +238,10 @@ struct CtaBand {
     for (int j0 = 0; j0 < n; j0 += NB) {
       const int nb = min(NB, n - j0);
       const int m = min(kd, n - j0 - nb);
+      if (kd < NB) {  // the previous step's prefetch overlaps this panel
+        cp_async_wait_all();
+        __syncthreads();
+      }
       if (threadIdx.x < 32) {
         const int f = potrf_diag(j0, nb);
         if (threadIdx.x == 0) s_fail = f;

@@ -1,0 +1,96 @@
+"""Quick device timings of the library entry points (CUDA events), for development.
+
+usage: python tools/timing.py [c5|single|all] [--batch B]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2305_04635_b200 as bc  # noqa: E402
+from paper_2305_04635_b200.inputs import CONFIGS, generate_spd, generate_spd_wide, make_rhs  # noqa: E402
+
+
+def timed(fn, reps=3):
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return min(ts), ts
+
+
+def c5(batch):
+    n, k = 4096, 100
+    ld = k + 1
+    a = np.stack([generate_spd(n, k, s).data for s in range(min(batch, 64))])
+    reps = (batch + a.shape[0] - 1) // a.shape[0]
+    a = np.concatenate([a] * reps)[:batch]
+    b = np.stack([make_rhs(n, s) for s in range(batch)])
+    a0 = torch.from_numpy(a).cuda()
+    b0 = torch.from_numpy(b).cuda()
+    w, wb = a0.clone(), b0.clone()
+    info = torch.zeros(batch, dtype=torch.int32, device="cuda")
+    flops = batch * n * k * (k + 3)
+
+    def fac():
+        w.copy_(a0)
+        torch.cuda.synchronize()
+        return bc.dpbtrf_batched_device(w, n, k, ld, batch, info=info)
+
+    def sv():
+        return bc.dpbsv_batched_device(w, n, k, ld, wb, batch, info=info)
+
+    def refresh():
+        w.copy_(a0); wb.copy_(b0)
+    out = {}
+    for name, f in (("dpbtrf_batched", lambda: bc.dpbtrf_batched_device(w, n, k, ld, batch, info=info)),
+                    ("dpbsv_batched", sv),
+                    ("dpbtrs_batched", lambda: bc.dpbtrs_batched_device(w, n, k, ld, wb, batch, info=info))):
+        ts = []
+        for _ in range(3):
+            refresh()
+            if name == "dpbtrs_batched":
+                bc.dpbtrf_batched_device(w, n, k, ld, batch, info=info)
+            torch.cuda.synchronize()
+            ms, _ = timed(f, 1)
+            ts.append(ms)
+        out[name] = {"ms": min(ts), "gflops": flops / (min(ts) * 1e-3) / 1e9}
+    assert int(info.abs().sum().item()) == 0
+    print(json.dumps({"c5_batch": batch, **out}), flush=True)
+
+
+def single(tags):
+    for tag in tags:
+        cfg = CONFIGS[tag]
+        n, k = cfg.dim, cfg.bandwidth
+        gen = generate_spd_wide if cfg.wide_diagonal else generate_spd
+        a0 = torch.from_numpy(gen(n, k, 0).data).cuda()
+        w = a0.clone()
+        info = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ts = []
+        for _ in range(3):
+            w.copy_(a0)
+            torch.cuda.synchronize()
+            ms, _ = timed(lambda: bc.dpbtrf_device(w, n, k, k + 1, info=info), 1)
+            ts.append(ms)
+        assert int(info.item()) == 0, int(info.item())
+        flops = n * k * (k + 3)
+        print(json.dumps({"config": tag, "factor_ms": min(ts), "gflops": flops / (min(ts) * 1e-3) / 1e9,
+                          "all_ms": ts}), flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    batch = int(sys.argv[sys.argv.index("--batch") + 1]) if "--batch" in sys.argv else 296
+    if what in ("c5", "all"):
+        c5(batch)
+    if what in ("single", "all"):
+        single(["C1", "C2", "C3", "C4"])
