@@ -75,6 +75,14 @@ int bcg_dpbtrs_batched(int64_t n, int64_t kd, const double* ab, int64_t ldab, in
 int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab,
                       double* b, int64_t stride_b, int64_t batch, int32_t* info, void* stream);
 
+/* Diagnostics: per-step phase timestamps of the whole-GPU factorization, the
+ * analogue of the reference's per-task trace (pkg/src/bandchol/parallel.py:54-62).
+ * Subsequent bcg_dpbtrf launches on the multi-CTA path write uint64 %globaltimer
+ * nanoseconds into device_buffer: [0] = steps recorded, then 8 stamps per block
+ * step (potrf start/end, L published, waits done, loads done, updates done,
+ * next panel published).  NULL disables tracing. */
+int bcg_set_trace(void* device_buffer, size_t bytes);
+
 /* Measurement utility (bench.py): FP64 FMA-pipe peak of the current device in
  * TFLOP/s, from a register-only DFMA loop over every SM (synchronous, ~10 ms).
  * The roofline denominator for the FP64-bound configs. */

@@ -27,6 +27,7 @@ SIGNATURES = {
     "bcg_dpbtrs_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _vp]),
     "bcg_dpbsv_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _vp]),
     "bcg_probe_fp64_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
+    "bcg_set_trace": (ctypes.c_int, [_vp, _sz]),
 }
 
 _lib = None

@@ -18,20 +18,21 @@
 namespace bcg {
 
 // One CTA per matrix (grid-stride over the batch).
-template <int NB, bool kWinSmem, bool kSolve>
+template <int NB, bool kSolve>
 __global__ void __launch_bounds__(kCtaThreads, 2)
 pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int batch, CtaGeom g,
-                 int32_t* info, double* pglob) {
+                 int32_t* info) {
   extern __shared__ __align__(16) double smem[];
   for (int mat = blockIdx.x; mat < batch; mat += gridDim.x) {
-    CtaBand<NB, kWinSmem, kSolve> w{g};
+    CtaBand<NB, kSolve> w{g};
     w.ab = ab0 + (int64_t)mat * stride_ab;
     w.rhs = kSolve ? b0 + (int64_t)mat * stride_b : nullptr;
     double* p = smem;
-    if (kWinSmem) { w.win = p; p += (size_t)g.nslot * g.lds; } else { w.win = nullptr; }
-    if (kWinSmem) { w.P = p; p += (size_t)NB * g.pld; } else { w.P = pglob + (size_t)blockIdx.x * NB * g.pld; }
+    w.win = p; p += (size_t)g.nslot * g.lds;
+    w.P = p; p += (size_t)NB * g.pld;
     w.D = p; p += NB * NB;
     w.Dinv = p; p += NB;
+    w.lbuf = p; p += 32;
     w.bw = kSolve ? p : nullptr;
     const int fail = w.factor();
     if (kSolve && fail < 0) w.backward();
@@ -54,6 +55,18 @@ pbtrs_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t stride_b,
   band_forward(ab, n, kd, ldab, b);
   band_backward(ab, n, kd, ldab, b);
   if (threadIdx.x == 0 && z % nrhs == 0) info[z / nrhs] = 0;
+}
+
+// Solve step of the unfused dpbsv path: matrices whose factorization failed keep info.
+__global__ void __launch_bounds__(kCtaThreads)
+pbtrs_after_factor_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int n, int kd,
+                          int ldab, const int32_t* info) {
+  const int z = blockIdx.x;
+  if (info[z] != 0) return;
+  const double* ab = ab0 + (int64_t)z * stride_ab;
+  double* b = b0 + (int64_t)z * stride_b;
+  band_forward(ab, n, kd, ldab, b);
+  band_backward(ab, n, kd, ldab, b);
 }
 
 }  // namespace bcg
@@ -104,72 +117,51 @@ bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb) {
   g.n = n;
   g.kd = kd;
   g.ldab = ldab;
-  g.lds = (kd + 1) | 1;  // odd column stride: element (i,j) has address parity of i
+  g.lds = (kd + 1) | 1;  // odd column stride
   int ns = kd + nb;
   if (ns & 1) ++ns;
   g.nslot = ns;
-  g.pld = ((kd + 3) / 4) * 4;
-  if (g.pld < 4) g.pld = 4;
+  int pld = ((kd + 15) / 16) * 16 + 4;  // covers the 16-row tiles, = 4 (mod 16)
+  g.pld = pld;
   return g;
 }
 
-template <int NB, bool W, bool S>
+// Block size for the one-CTA-per-matrix kernel: the largest NB whose window fits
+// two CTAs per SM, else one; 0 if the window does not fit at all.
+int cta_block(int n, int kd, int ldab, bool solve, bcg::CtaGeom* out) {
+  const size_t limit = (size_t)smem_optin();
+  const size_t half = 113 * 1024;
+  for (size_t cap : {half, limit}) {
+    for (int nb : {16, 32}) {
+      bcg::CtaGeom g = make_geom(n, kd, ldab, nb);
+      if (bcg::cta_smem_bytes(nb, g, solve) > cap) continue;
+      if (solve && g.nslot < 5 * nb) continue;  // backward-sweep prefetch ring needs 5 blocks
+      *out = g;
+      return nb;
+    }
+  }
+  return 0;
+}
+
+template <int NB, bool S>
 int launch_cta_t(double* ab, int64_t sab, double* b, int64_t sb, int batch, const bcg::CtaGeom& g, int32_t* info,
-                 cudaStream_t st, double* pglob = nullptr, int grid = 0) {
-  const size_t smem = bcg::cta_smem_bytes(NB, g, W, S);
-  auto k = bcg::pbtrf_cta_kernel<NB, W, S>;
+                 cudaStream_t st) {
+  const size_t smem = bcg::cta_smem_bytes(NB, g, S);
+  auto k = bcg::pbtrf_cta_kernel<NB, S>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
-  if (grid <= 0) grid = batch;
-  k<<<grid, bcg::kCtaThreads, smem, st>>>(ab, sab, b, sb, batch, g, info, pglob);
+  k<<<batch, bcg::kCtaThreads, smem, st>>>(ab, sab, b, sb, batch, g, info);
   return cuda_status(cudaGetLastError(), "pbtrf_cta_kernel launch");
 }
 
-// Global-window variant: persistent grid, per-CTA panel scratch.  The scratch is
-// either the caller's workspace (bcg_dpbtrf) or stream-ordered (cudaMallocAsync).
-template <bool S>
-int launch_cta_global(double* ab, int64_t sab, double* b, int64_t sb, int batch, const bcg::CtaGeom& g,
-                      int32_t* info, cudaStream_t st, double* scratch) {
-  const int grid = batch < 2 * sm_count() ? batch : 2 * sm_count();
-  double* pg = scratch;
-  if (!pg) {
-    cudaError_t e = cudaMallocAsync((void**)&pg, (size_t)grid * 32 * g.pld * sizeof(double), st);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(panel scratch)");
-  }
-  int r = launch_cta_t<32, false, S>(ab, sab, b, sb, batch, g, info, st, pg, scratch ? 1 : grid);
-  if (!scratch) cudaFreeAsync(pg, st);
-  return r;
-}
-
-// Pick the block size and window placement for the one-CTA-per-matrix kernel.
-int launch_cta(double* ab, int64_t sab, double* b, int64_t sb, int batch, int n, int kd, int ldab, int32_t* info,
-               bool solve, cudaStream_t st, double* scratch = nullptr) {
-  const size_t limit = (size_t)smem_optin();
-  // Prefer two resident CTAs per SM (<= half the SM's shared memory), then one.
-  const size_t half = 113 * 1024;
-  const int cands[3] = {16, 32, 8};
-  for (size_t cap : {half, limit}) {
-    for (int nb : cands) {
-      bcg::CtaGeom g = make_geom(n, kd, ldab, nb);
-      if (bcg::cta_smem_bytes(nb, g, true, solve) > cap) continue;
-      if (solve) {
-        if (nb == 16) return launch_cta_t<16, true, true>(ab, sab, b, sb, batch, g, info, st);
-        if (nb == 32) return launch_cta_t<32, true, true>(ab, sab, b, sb, batch, g, info, st);
-        return launch_cta_t<8, true, true>(ab, sab, b, sb, batch, g, info, st);
-      }
-      if (nb == 16) return launch_cta_t<16, true, false>(ab, sab, b, sb, batch, g, info, st);
-      if (nb == 32) return launch_cta_t<32, true, false>(ab, sab, b, sb, batch, g, info, st);
-      return launch_cta_t<8, true, false>(ab, sab, b, sb, batch, g, info, st);
-    }
-  }
-  // Window too large for shared memory: run in place on the band in global memory.
-  bcg::CtaGeom g = make_geom(n, kd, ldab, 32);
+int launch_cta(double* ab, int64_t sab, double* b, int64_t sb, int batch, int nb, const bcg::CtaGeom& g,
+               int32_t* info, bool solve, cudaStream_t st) {
   if (solve) {
-    if (bcg::cta_smem_bytes(32, g, false, true) <= limit)
-      return launch_cta_global<true>(ab, sab, b, sb, batch, g, info, st, scratch);
-    return fail_arg(2, "kd=%d too large for the fused batched solve; use dpbtrf_batched + dpbtrs_batched", kd);
+    if (nb == 16) return launch_cta_t<16, true>(ab, sab, b, sb, batch, g, info, st);
+    return launch_cta_t<32, true>(ab, sab, b, sb, batch, g, info, st);
   }
-  return launch_cta_global<false>(ab, sab, b, sb, batch, g, info, st, scratch);
+  if (nb == 16) return launch_cta_t<16, false>(ab, sab, b, sb, batch, g, info, st);
+  return launch_cta_t<32, false>(ab, sab, b, sb, batch, g, info, st);
 }
 
 int check_geom(int64_t n, int64_t kd, int64_t ldab) {
@@ -187,17 +179,17 @@ int bcg_version(void) { return 100; }
 
 const char* bcg_last_error(void) { return g_err; }
 
-// Bytes of panel scratch the one-CTA global-window variant needs (0 if the window fits in smem).
-static size_t cta_scratch_bytes(int n, int kd, int ldab) {
-  bcg::CtaGeom g = make_geom(n, kd, ldab, 8);
-  if (bcg::cta_smem_bytes(8, g, true, false) <= (size_t)smem_optin()) return 0;
-  return (size_t)32 * make_geom(n, kd, ldab, 32).pld * sizeof(double);
+// Single matrices: one CTA when the window fits in shared memory, else the
+// whole-GPU dataflow kernel (which needs the caller's workspace).
+static bool single_uses_multi(int n, int kd, int ldab) {
+  bcg::CtaGeom g;
+  return cta_block(n, kd, ldab, false, &g) == 0 || bcg::use_multi(n, kd);
 }
 
 size_t bcg_dpbtrf_workspace_size(int64_t n, int64_t kd, int64_t ldab) {
   if (check_geom(n, kd, ldab) != 0) return 0;
-  if (bcg::use_multi((int)n, (int)kd)) return bcg::multi_workspace_bytes((int)n, (int)kd);
-  return cta_scratch_bytes((int)n, (int)kd, (int)ldab);
+  if (!single_uses_multi((int)n, (int)kd, (int)ldab)) return 0;
+  return bcg::multi_workspace_bytes((int)n, (int)kd);
 }
 
 int bcg_dpbtrf(int64_t n, int64_t kd, double* ab, int64_t ldab, int32_t* info, void* workspace,
@@ -206,17 +198,30 @@ int bcg_dpbtrf(int64_t n, int64_t kd, double* ab, int64_t ldab, int32_t* info, v
   if (!ab) return fail_arg(3, "ab is NULL");
   if (!info) return fail_arg(5, "info is NULL");
   cudaStream_t st = (cudaStream_t)stream;
-  if (bcg::use_multi((int)n, (int)kd)) {
+  if (single_uses_multi((int)n, (int)kd, (int)ldab)) {
     const size_t need = bcg::multi_workspace_bytes((int)n, (int)kd);
     if (!workspace || workspace_bytes < need)
       return fail_arg(6, "workspace of %zu bytes required (got %zu)", need, workspace_bytes);
     return bcg::launch_multi(ab, (int)n, (int)kd, (int)ldab, info, workspace, sm_count(), st, g_err, sizeof g_err);
   }
-  const size_t need = cta_scratch_bytes((int)n, (int)kd, (int)ldab);
-  if (need && (!workspace || workspace_bytes < need))
-    return fail_arg(6, "workspace of %zu bytes required (got %zu)", need, workspace_bytes);
-  return launch_cta(ab, 0, nullptr, 0, 1, (int)n, (int)kd, (int)ldab, info, false, st,
-                    need ? (double*)workspace : nullptr);
+  bcg::CtaGeom g;
+  const int nb = cta_block((int)n, (int)kd, (int)ldab, false, &g);
+  return launch_cta(ab, 0, nullptr, 0, 1, nb, g, info, false, st);
+}
+
+// Batched matrices whose window does not fit one CTA: one whole-GPU factorization
+// after another, with a stream-ordered workspace.
+static int batched_multi(int n, int kd, int ldab, double* ab, int64_t stride_ab, int batch, int32_t* info,
+                         cudaStream_t st) {
+  const size_t need = bcg::multi_workspace_bytes(n, kd);
+  void* ws = nullptr;
+  if (int r = cuda_status(cudaMallocAsync(&ws, need, st), "cudaMallocAsync(workspace)")) return r;
+  int rc = 0;
+  for (int i = 0; i < batch && rc == 0; ++i)
+    rc = bcg::launch_multi(ab + (int64_t)i * stride_ab, n, kd, ldab, info + i, ws, sm_count(), st, g_err,
+                           sizeof g_err);
+  cudaFreeAsync(ws, st);
+  return rc;
 }
 
 int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, int64_t batch,
@@ -227,9 +232,14 @@ int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t 
   if (batch < 0 || batch > INT_MAX) return fail_arg(6, "batch out of range");
   if (!info) return fail_arg(7, "info is NULL");
   if (batch == 0) return 0;
-  return launch_cta(ab, stride_ab, nullptr, 0, (int)batch, (int)n, (int)kd, (int)ldab, info, false,
-                    (cudaStream_t)stream);
+  bcg::CtaGeom g;
+  const int nb = cta_block((int)n, (int)kd, (int)ldab, false, &g);
+  if (nb == 0) return batched_multi((int)n, (int)kd, (int)ldab, ab, stride_ab, (int)batch, info, (cudaStream_t)stream);
+  return launch_cta(ab, stride_ab, nullptr, 0, (int)batch, nb, g, info, false, (cudaStream_t)stream);
 }
+
+static int launch_solve(const double* ab, int64_t sab, double* b, int64_t sb, int nrhs, int64_t blocks, int n,
+                        int kd, int ldab, int32_t* info, cudaStream_t st);
 
 int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, double* b,
                       int64_t stride_b, int64_t batch, int32_t* info, void* stream) {
@@ -241,8 +251,16 @@ int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t s
   if (batch < 0 || batch > INT_MAX) return fail_arg(8, "batch out of range");
   if (!info) return fail_arg(9, "info is NULL");
   if (batch == 0) return 0;
-  return launch_cta(ab, stride_ab, b, stride_b, (int)batch, (int)n, (int)kd, (int)ldab, info, true,
-                    (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  bcg::CtaGeom g;
+  const int nb = cta_block((int)n, (int)kd, (int)ldab, true, &g);
+  if (nb) return launch_cta(ab, stride_ab, b, stride_b, (int)batch, nb, g, info, true, st);
+  // no fused variant for this geometry: factor, then solve (solve skips failed matrices)
+  int rc = bcg_dpbtrf_batched(n, kd, ab, ldab, stride_ab, batch, info, stream);
+  if (rc) return rc;
+  bcg::pbtrs_after_factor_kernel<<<(unsigned)batch, bcg::kCtaThreads, 0, st>>>(ab, stride_ab, b, stride_b, (int)n,
+                                                                             (int)kd, (int)ldab, info);
+  return cuda_status(cudaGetLastError(), "pbtrs_after_factor_kernel launch");
 }
 
 static int launch_solve(const double* ab, int64_t sab, double* b, int64_t sb, int nrhs, int64_t blocks, int n,
@@ -298,6 +316,13 @@ __global__ void __launch_bounds__(512) dfma_probe_kernel(double* out, int iters)
   if (s == 12345.678) out[0] = s;
 }
 }  // namespace bcg
+
+extern "C" int bcg_set_trace(void* device_buffer, size_t bytes) {
+  unsigned long long* p = (unsigned long long*)device_buffer;
+  unsigned long long cap = device_buffer ? bytes / sizeof(unsigned long long) : 0;
+  if (int r = cuda_status(cudaMemcpyToSymbol(bcg::g_trace, &p, sizeof p), "cudaMemcpyToSymbol(trace)")) return r;
+  return cuda_status(cudaMemcpyToSymbol(bcg::g_trace_cap, &cap, sizeof cap), "cudaMemcpyToSymbol(trace cap)");
+}
 
 extern "C" int bcg_probe_fp64_peak(double* tflops) {
   if (!tflops) return fail_arg(1, "tflops is NULL");

@@ -94,3 +94,39 @@ if __name__ == "__main__":
         c5(batch)
     if what in ("single", "all"):
         single(["C1", "C2", "C3", "C4"])
+
+
+def trace(tag):
+    """Pivot phase breakdown of the multi-CTA kernel (bcg_set_trace)."""
+    from paper_2305_04635_b200 import _lib
+    cfg = CONFIGS[tag]
+    n, k = cfg.dim, cfg.bandwidth
+    gen = generate_spd_wide if cfg.wide_diagonal else generate_spd
+    a0 = torch.from_numpy(gen(n, k, 0).data).cuda()
+    buf = torch.zeros(1 + 8 * (n // 16 + 2), dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    w = a0.clone()
+    bc.dpbtrf_device(w, n, k, k + 1)
+    torch.cuda.synchronize()
+    lib.bcg_set_trace(buf.data_ptr(), buf.numel() * 8)
+    w = a0.clone()
+    bc.dpbtrf_device(w, n, k, k + 1)
+    torch.cuda.synchronize()
+    lib.bcg_set_trace(None, 0)
+    t = buf.cpu().numpy()
+    steps = int(t[0])
+    st = t[1:1 + 8 * steps].reshape(steps, 8).astype(np.float64)
+    d = np.diff(st[:, :7], axis=1)  # phase durations 0->1 .. 5->6
+    nxt = st[1:, 0] - st[:-1, 6]     # gap to next step start
+    names = ["potrf_inv", "store_publish", "wait", "load", "gemm", "publish_next"]
+    out = {"config": tag, "steps": steps, "total_ms": float((st[-1, 1] - st[0, 0]) / 1e6)}
+    for i, nm in enumerate(names):
+        v = d[:-1, i]
+        out[nm + "_us"] = float(np.median(v) / 1e3)
+    out["gap_us"] = float(np.median(nxt) / 1e3)
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace":
+    for tg in sys.argv[2:] or ["C2", "C3", "C4"]:
+        trace(tg)
