@@ -47,10 +47,82 @@ __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// ---- bulk async copies (TMA bulk path, SASS UBLKCP) + mbarriers -------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// global -> shared, completion counted on `bar` (bytes % 16 == 0, both addresses 16-aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// shared -> global (bulk group)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// make this thread's generic-proxy shared-memory writes visible to the async proxy
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// ---- optional trace (bcg_set_trace): phase stamps, %globaltimer ns -------------
+// [0] = steps recorded, then kTracePhases stamps per step (block 0 / matrix 0 only
+// for this kernel; the pivot CTA for the multi-CTA kernel).
+constexpr int kTracePhases = 8;
+__device__ unsigned long long* g_trace = nullptr;
+__device__ unsigned long long g_trace_cap = 0;
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));  // SM cycles: phases of one CTA
+  return t;
+}
+__device__ __forceinline__ void trace_stamp_to(unsigned long long* tr, int j, int phase) {
+  if (tr) {
+    const unsigned long long idx = 1 + (unsigned long long)j * kTracePhases + phase;
+    if (idx < g_trace_cap) tr[idx] = gtime();
+    if (phase == 0 && (unsigned long long)j + 1 > tr[0]) tr[0] = j + 1;
+  }
+}
+
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+// Branch-free full-precision 1/sqrt(p) for finite p > 0: MUFU.RSQ64H seed + two
+// Newton steps (relative error ~2^-44 after the first, rounding-limited after the
+// second).  No special-case branch, so the compiler can interleave it with the
+// surrounding work; non-positive / NaN pivots are caught by the caller's check.
+__device__ __forceinline__ double rsqrt_nr(double p) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
+  double h = p * y;
+  double e = fma(-h, y, 1.0);
+  y = fma(y * 0.5, e, y);
+  h = p * y;
+  e = fma(-h, y, 1.0);
+  y = fma(y * 0.5, e, y);
+  return y;
 }
 
 struct CtaGeom {
@@ -62,7 +134,7 @@ struct CtaGeom {
 // Shared-memory footprint (bytes) of one CTA for block size NB.
 __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g, bool solve) {
   size_t d = (size_t)g.nslot * g.lds + (size_t)nb_block * g.pld + (size_t)nb_block * nb_block + nb_block + 32;
-  if (solve) d += (size_t)g.nslot;  // ring of right-hand-side entries
+  if (solve) d += (size_t)g.nslot + (size_t)(g.nslot / nb_block) * nb_block;  // rhs ring + staged y
   return d * sizeof(double) + 64;
 }
 
@@ -74,10 +146,21 @@ struct CtaBand {
   double* __restrict__ rhs;  // its right-hand side (kSolve)
   double* win;               // shared ring of column slots
   double* P;                 // NB x pld dense panel, P[c*pld + r] = L(j0+nb+r, j0+c)
-  double* D;                 // NB x NB dense L11, row-major
+  double* D;                 // NB x NB dense L11, D[c*NB + r] = L(r, c)
   double* Dinv;              // NB reciprocals of diag(L11)
   double* lbuf;              // 32 doubles: column broadcast inside the POTRF warp
   double* bw;                // ring of rhs / solution entries, slot(i) like columns
+  double* yb;                // backward sweep: nbuf x NB staged y entries
+  unsigned long long* bars;  // mbarriers: [0] window loads, [1 + k] backward buffer k
+  unsigned* bphase;          // smem: parity of the next wait on bars[1 + k]
+  unsigned phase = 0;        // parity of the next wait on bars[0] (uniform register)
+  bool pending = false;      // a load_cols is in flight
+  bool fast = false;         // every column chunk meets the bulk-copy alignment rules
+  unsigned long long* tr = nullptr;  // trace buffer (block 0 only), see bcg_set_trace
+
+  __device__ __forceinline__ void trace_stamp(int j, int ph) const {
+    if (tr && (threadIdx.x & 31) == 0) trace_stamp_to(tr, j, ph);
+  }
 
   // ---- ring addressing: slot(j) = j mod nslot without a division on hot paths ----
   __device__ __forceinline__ int slot_from(int s0, int j0, int j) const {
@@ -86,34 +169,142 @@ struct CtaBand {
   }
   __device__ __forceinline__ int col_len(int j) const { return min(g.kd, g.n - 1 - j) + 1; }
 
-  // cp.async columns [jlo, jhi) (and their rhs entries) into the ring.
+  // ---- column streaming between HBM and the ring -----------------------------------
+  // Whole columns (ldab doubles, padding included, so the write-back restores the
+  // padding bytes unchanged) move as bulk async copies in contiguous chunks; a column
+  // whose chunk would break the 16-byte rules of cp.async.bulk goes element-wise.
+  // Plan for columns [jlo, jhi) placed at ring slot (jlo % nslot) onward: up to two
+  // contiguous pieces (ring wrap), each trimmed to an aligned bulk range.
+  struct Piece { int j, cnt, slot; };
+  __device__ __forceinline__ int pieces(int jlo, int jhi, Piece* pc) const {
+    const int s0 = jlo % g.nslot;
+    const int c1 = min(jhi - jlo, g.nslot - s0);
+    pc[0] = {jlo, c1, s0};
+    if (c1 < jhi - jlo) { pc[1] = {jlo + c1, jhi - jlo - c1, 0}; return 2; }
+    return 1;
+  }
+  // bulk sub-range [b0, b0+bc) of a piece; columns outside it go element-wise
+  __device__ __forceinline__ void bulk_range(const Piece& p, const double* gbase, int& b0, int& bc) const {
+    auto aligned = [&](int c) {
+      return !(((uintptr_t)(gbase + (int64_t)(p.j + c) * g.ldab)) & 15) &&
+             !(((uintptr_t)(win + (size_t)(p.slot + c) * g.lds)) & 15);
+    };
+    b0 = aligned(0) ? 0 : 1;  // odd start with odd ldab: the next column is aligned on both sides
+    if (b0 >= p.cnt || !aligned(b0)) {
+      b0 = 0;
+      bc = 0;
+      return;
+    }
+    bc = p.cnt - b0;
+    if (((size_t)bc * g.ldab * sizeof(double)) % 16) bc -= 1;
+  }
+  __device__ void elem_copy_col(int j, int slot, bool to_smem) {
+    double* sp = win + (size_t)slot * g.lds;
+    double* gp = ab + (int64_t)j * g.ldab;
+    for (int o = threadIdx.x; o < g.ldab; o += kCtaThreads) {
+      if (to_smem) cp_async8(sp + o, gp + o);
+      else gp[o] = sp[o];
+    }
+  }
+
+  // The fast path holds when the matrix base is 16-byte aligned and every chunk the
+  // kernel moves starts on an even column with an even count or ldab is even
+  // (decided once per matrix by the host-chosen geometry, see init_fast()).
+  __device__ void init_fast() {
+    fast = !(((uintptr_t)ab) & 15) && !(((uintptr_t)win) & 15) && ((g.ldab % 2 == 0) || (g.nslot % 2 == 0 && g.kd % 2 == 0));
+    // with odd ldab the chunks start at j0 + NB + kd (even) and the tail count n - jlo must be even
+    if (fast && g.ldab % 2 == 1) fast = ((g.n - min(g.n, g.kd + NB)) % 2 == 0) && (min(g.n, g.kd + NB) % 2 == 0);
+  }
+
+  // async load of columns [jlo, jhi) (and their rhs entries); complete with wait_cols()
   __device__ void load_cols(int jlo, int jhi) {
-    const int per = g.kd + 1;
-    const int total = (jhi - jlo) * per;
-    for (int idx = threadIdx.x; idx < total; idx += kCtaThreads) {
-      const int c = idx / per, o = idx - c * per;
-      const int j = jlo + c;
-      if (o < col_len(j)) cp_async8(win + (j % g.nslot) * g.lds + o, ab + (int64_t)j * g.ldab + o);
+    if (fast) {
+      if (threadIdx.x == 0) {
+        bulk_wait_read0();  // the write-back that read these slots is done reading
+        const unsigned col = (unsigned)g.ldab * sizeof(double);
+        mbar_expect_tx(bars, (unsigned)(jhi - jlo) * col);
+        const int s0 = jlo % g.nslot;
+        const int c1 = min(jhi - jlo, g.nslot - s0);
+        bulk_g2s(win + (size_t)s0 * g.lds, ab + (int64_t)jlo * g.ldab, c1 * col, bars);
+        if (c1 < jhi - jlo) bulk_g2s(win, ab + (int64_t)(jlo + c1) * g.ldab, (jhi - jlo - c1) * col, bars);
+      }
+      if (kSolve) {
+        for (int j = jlo + threadIdx.x; j < jhi; j += kCtaThreads) cp_async8(bw + (j % g.nslot), rhs + j);
+        cp_async_commit();
+      }
+      pending = true;
+      return;
+    }
+    if (threadIdx.x == 0) bulk_wait_read0();  // the write-back that read these slots is done reading
+    __syncthreads();
+    Piece pc[2];
+    const int np = pieces(jlo, jhi, pc);
+    unsigned bytes = 0;
+    for (int q = 0; q < np; ++q) {
+      int b0, bc;
+      bulk_range(pc[q], ab, b0, bc);
+      bytes += (unsigned)bc * g.ldab * sizeof(double);
+      for (int c = 0; c < pc[q].cnt; ++c)
+        if (c < b0 || c >= b0 + bc) elem_copy_col(pc[q].j + c, pc[q].slot + c, true);
+    }
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bars, bytes);
+      for (int q = 0; q < np; ++q) {
+        int b0, bc;
+        bulk_range(pc[q], ab, b0, bc);
+        if (bc > 0)
+          bulk_g2s(win + (size_t)(pc[q].slot + b0) * g.lds, ab + (int64_t)(pc[q].j + b0) * g.ldab,
+                   (unsigned)bc * g.ldab * sizeof(double), bars);
+      }
     }
     if (kSolve)
       for (int j = jlo + threadIdx.x; j < jhi; j += kCtaThreads) cp_async8(bw + (j % g.nslot), rhs + j);
     cp_async_commit();
+    pending = true;
+  }
+  // all threads: the last load_cols has landed and is visible
+  __device__ __forceinline__ void wait_cols() {
+    if (kSolve || !fast) cp_async_wait_all();
+    mbar_wait(bars, phase);
+    phase ^= 1u;
+    pending = false;
+    __syncthreads();
   }
 
-  // Panel columns [j0, j0+nb) back to HBM (final L).
-  __device__ void store_cols(int s0, int j0, int nb) {
-    const int per = g.kd + 1;
-    const int total = nb * per;
-    for (int idx = threadIdx.x; idx < total; idx += kCtaThreads) {
-      const int c = idx / per, o = idx - c * per;
-      const int j = j0 + c;
-      if (o < col_len(j)) ab[(int64_t)j * g.ldab + o] = win[slot_from(s0, j0, j) * g.lds + o];
+  // Panel columns [j0, j0+nb) back to HBM (final L).  Call after a barrier that
+  // follows fence_async_smem() by every writer; the bulk part is issued by thread 0.
+  __device__ void store_cols(int j0, int nb) {
+    if (fast) {
+      if (threadIdx.x == 0) {
+        const unsigned col = (unsigned)g.ldab * sizeof(double);
+        const int s0 = j0 % g.nslot;
+        const int c1 = min(nb, g.nslot - s0);
+        bulk_s2g(ab + (int64_t)j0 * g.ldab, win + (size_t)s0 * g.lds, c1 * col);
+        if (c1 < nb) bulk_s2g(ab + (int64_t)(j0 + c1) * g.ldab, win, (nb - c1) * col);
+        bulk_commit();
+      }
+      return;
     }
+    Piece pc[2];
+    const int np = pieces(j0, j0 + nb, pc);
+    for (int q = 0; q < np; ++q) {
+      int b0, bc;
+      bulk_range(pc[q], ab, b0, bc);
+      for (int c = 0; c < pc[q].cnt; ++c)
+        if (c < b0 || c >= b0 + bc) elem_copy_col(pc[q].j + c, pc[q].slot + c, false);
+      if (threadIdx.x == 0 && bc > 0)
+        bulk_s2g(ab + (int64_t)(pc[q].j + b0) * g.ldab, win + (size_t)(pc[q].slot + b0) * g.lds,
+                 (unsigned)bc * g.ldab * sizeof(double));
+    }
+    if (threadIdx.x == 0) bulk_commit();
   }
 
   // Warp 0: Cholesky of the nb x nb diagonal block at column j0 (+ forward sweep).
   // Lane r holds row r.  Returns the local failing column or -1 (uniform).
+  // kFull (nb == NB, every block but possibly the last) compiles to straight-line code.
+  template <bool kWhole>
   __device__ int potrf_diag(int s0, int j0, int nb) {
+    if (kWhole) nb = NB;
     const int r = threadIdx.x & 31;
     double row[NB];
 #pragma unroll
@@ -121,43 +312,51 @@ struct CtaBand {
       row[c] = (r < nb && c <= r && r - c <= g.kd) ? win[slot_from(s0, j0, j0 + c) * g.lds + (r - c)] : 0.0;
     double s = 0.0;
     if (kSolve && r < nb) s = bw[slot_from(s0, j0, j0 + r)];
-    // chain state, identical in every lane
+    // chain state, identical in every lane: p = pivot of column c, (alpha, beta) =
+    // (A'(c+1,c), A'(c+1,c+1)) through column c-1, broadcast by lane c+1 a step early.
     double p = __shfl_sync(kFull, row[0], 0);
-    double alpha = __shfl_sync(kFull, row[0], 1);  // A'(1,0)
-    double beta = __shfl_sync(kFull, row[1], 1);   // A'(1,1)
+    double alpha = __shfl_sync(kFull, row[0], 1);
+    double beta = __shfl_sync(kFull, row[1], 1);
+    double rs = rsqrt_nr(p);
     double myinv = 0.0;
     int fail = -1;
+    // Software-pipelined: the next column's 1/sqrt and chain broadcasts are issued
+    // before this column's rank-1 update, so their latency hides under it.
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
-      if (c < nb) {
-        if (!(p > 0.0)) { fail = c; break; }
-        const double rs = rsqrt(p);
-        const double lrc = row[c] * rs;     // L(r, c) for r > c
-        const double l1 = alpha * rs;       // L(c+1, c), known to every lane
-        const double pn = fma(-l1, l1, beta);
-        if (r == c) { row[c] = p * rs; myinv = rs; }
-        else if (r > c) row[c] = lrc;
-        if (kSolve) {
-          const double yc = __shfl_sync(kFull, s, c) * rs;
-          if (r == c) s = yc;
-          else if (r > c) s = fma(-lrc, yc, s);
-        }
-        lbuf[r] = (r > c) ? lrc : 0.0;
-        __syncwarp();
-        if (r > c) {
-#pragma unroll
-          for (int c2 = c + 1; c2 < NB; ++c2) {
-            const double lc2 = (c2 == c + 1) ? l1 : ((c2 == r) ? lrc : lbuf[c2]);
-            if (r >= c2) row[c2] = fma(-lrc, lc2, row[c2]);
-          }
-        }
-        __syncwarp();
-        if (c + 2 < NB) {
-          alpha = __shfl_sync(kFull, row[c + 1 < NB ? c + 1 : 0], c + 2);
-          beta = __shfl_sync(kFull, row[c + 2 < NB ? c + 2 : 0], c + 2);
-        }
-        p = pn;
+      const bool act = kWhole || c < nb;
+      if (act && fail < 0 && !(p > 0.0)) fail = c;
+      const double lrc = (r > c) ? row[c] * rs : 0.0;  // L(r, c); 0 on and above the diagonal
+      const double l1 = alpha * rs;                     // L(c+1, c)
+      const double pn = fma(-l1, l1, beta);             // pivot of column c+1
+      const double rsn = rsqrt_nr(pn);
+      // entry (r, c+1) first, with L(c+1,c) = l1 from registers: the next column's
+      // L(r, c+1) never waits on the shared-memory broadcast below
+      if (c + 1 < NB) row[c + 1 < NB ? c + 1 : 0] = fma(-lrc, l1, row[c + 1 < NB ? c + 1 : 0]);
+      double alpha_n = 0.0, beta_n = 0.0;
+      if (c + 2 < NB) {
+        // lane c+2's entries (c+2, c+1), (c+2, c+2) after this column
+        const double bn = fma(-lrc, lrc, row[c + 2 < NB ? c + 2 : 0]);
+        alpha_n = __shfl_sync(kFull, row[c + 1 < NB ? c + 1 : 0], c + 2);
+        beta_n = __shfl_sync(kFull, bn, c + 2);
       }
+      if (kSolve) {
+        const double yc = __shfl_sync(kFull, s, c) * rs;
+        if (act) s = (r == c) ? yc : fma(-lrc, yc, s);
+      }
+      if (r == c) { row[c] = p * rs; myinv = rs; }
+      else if (r > c) row[c] = lrc;
+      lbuf[r] = lrc;
+      __syncwarp();
+      // rank-1 update of the rest of the row; entries right of the diagonal become
+      // garbage that is never read (only c2 <= r is used or stored)
+#pragma unroll
+      for (int c2 = c + 2; c2 < NB; ++c2) row[c2] = fma(-lrc, lbuf[c2], row[c2]);
+      __syncwarp();
+      p = pn;
+      rs = rsn;
+      alpha = alpha_n;
+      beta = beta_n;
     }
     if (fail < 0) {
       if (r < nb) {
@@ -171,7 +370,7 @@ struct CtaBand {
       }
       if (r < NB) {
 #pragma unroll
-        for (int c = 0; c < NB; ++c) D[r * NB + c] = (r < nb && c <= r) ? row[c] : 0.0;
+        for (int c = 0; c < NB; ++c) D[c * NB + r] = (r < nb && c <= r) ? row[c] : 0.0;  // D[c][r] = L(r, c)
         Dinv[r] = r < nb ? myinv : 0.0;
       }
     }
@@ -182,23 +381,21 @@ struct CtaBand {
   __device__ void trsm_panel(int s0, int j0, int nb, int m) {
     for (int r = threadIdx.x; r < m; r += kCtaThreads) {
       double x[NB];
-      int sl[NB];
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         const int off = nb + r - c;
-        sl[c] = slot_from(s0, j0, j0 + (c < nb ? c : 0)) * g.lds + off;
-        x[c] = (c < nb && off <= g.kd) ? win[sl[c]] : 0.0;
+        x[c] = (c < nb && off <= g.kd) ? win[slot_from(s0, j0, j0 + c) * g.lds + off] : 0.0;
       }
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         x[c] *= Dinv[c];
 #pragma unroll
-        for (int c2 = c + 1; c2 < NB; ++c2) x[c2] = fma(-x[c], D[c2 * NB + c], x[c2]);
+        for (int c2 = c + 1; c2 < NB; ++c2) x[c2] = fma(-x[c], D[c * NB + c2], x[c2]);
       }
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         const int off = nb + r - c;
-        if (c < nb && off <= g.kd) win[sl[c]] = x[c];
+        if (c < nb && off <= g.kd) win[slot_from(s0, j0, j0 + c) * g.lds + off] = x[c];
         P[c * g.pld + r] = x[c];
       }
     }
@@ -206,9 +403,12 @@ struct CtaBand {
 
   // Trailing update of 16x16 tiles (ti >= tj) with tile column tj in [tj_lo, tj_hi),
   // by warps [w_lo, kCtaWarps).  C(i,j) -= sum_c P(i,c) P(j,c), i,j < m, lower only.
+  // w_lo == 1: the lookahead phase, run by warps 1-3 and 5-7 so that SMSP 0 (warps 0
+  // and 4) is left to the POTRF warp.
   __device__ void update_tiles(int s0, int j0, int nb, int m, int tj_lo, int tj_hi, int w_lo) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp < w_lo) return;
+    if (warp < w_lo || (w_lo == 1 && warp == 4)) return;
+    const int wid = (w_lo == 1) ? (warp < 4 ? warp - 1 : warp - 2) : warp;  // rank among the workers
     const int gr = lane >> 2, gc = lane & 3;
     const int base = j0 + nb;
     const int T = (m + 15) >> 4;
@@ -217,8 +417,8 @@ struct CtaBand {
     // tiles of columns [tj_lo, tj_hi): column tj holds T - tj tiles
     const int first = tj_lo * T - tj_lo * (tj_lo - 1) / 2;
     const int last = tj_hi * T - tj_hi * (tj_hi - 1) / 2;
-    const int nw = kCtaWarps - w_lo;
-    for (int t = first + (warp - w_lo); t < last; t += nw) {
+    const int nw = (w_lo == 1) ? kCtaWarps - 2 : kCtaWarps;
+    for (int t = first + wid; t < last; t += nw) {
       int tj = tj_lo;
       while (tj + 1 < tj_hi && (tj + 1) * T - (tj + 1) * tj / 2 <= t) ++tj;
       const int ti = tj + (t - (tj * T - tj * (tj - 1) / 2));
@@ -277,90 +477,117 @@ struct CtaBand {
     const int n = g.n, kd = g.kd;
     __shared__ int s_fail;
     const int warp = threadIdx.x >> 5;
+    init_fast();
     // zero the panel buffer once (rows past m are read, never used, by the tile GEMM)
     for (int idx = threadIdx.x; idx < NB * g.pld; idx += kCtaThreads) P[idx] = 0.0;
     load_cols(0, min(n, kd + NB));
-    cp_async_wait_all();
-    __syncthreads();
+    wait_cols();
     if (warp == 0) {
-      const int f = potrf_diag(0, 0, min(NB, n));
+      const int f = (n >= NB) ? potrf_diag<true>(0, 0, NB) : potrf_diag<false>(0, 0, n);
       if (threadIdx.x == 0) s_fail = f;
     }
     __syncthreads();
-    if (s_fail >= 0) return s_fail;
+    if (s_fail >= 0) {
+      drain();
+      return s_fail;
+    }
     int j0 = 0, s0 = 0;
     for (;;) {
       const int nb = min(NB, n - j0);
       const int m = min(kd, n - j0 - nb);
+      const int step = j0 / NB;
+      if (threadIdx.x < 32) trace_stamp(step, 0);
       trsm_panel(s0, j0, nb, m);
-      cp_async_wait_all();  // columns prefetched by the previous step
-      __syncthreads();
-      store_cols(s0, j0, nb);
+      if (threadIdx.x < 32) trace_stamp(step, 7);
+      fence_async_smem();  // panel writes -> visible to the bulk write-back
+      if (pending) wait_cols();  // columns prefetched by the previous step
+      else __syncthreads();
+      if (threadIdx.x < 32) trace_stamp(step, 1);
+      store_cols(j0, nb);
       // part 1: tile columns touching the next panel, then the rhs
       update_tiles(s0, j0, nb, m, 0, NB / 16, 0);
       if (kSolve) update_rhs(s0, j0, nb, m);
       __syncthreads();
+      if (threadIdx.x < 32) trace_stamp(step, 2);
       const int jlo = j0 + NB + kd;
       if (jlo < n) load_cols(jlo, min(n, jlo + NB));
       const int j1 = j0 + nb;
       if (j1 >= n) break;
       int s1 = s0 + nb;
       if (s1 >= g.nslot) s1 -= g.nslot;
-      if (kd < NB) {  // the prefetch just issued overlaps the next panel
-        cp_async_wait_all();
-        __syncthreads();
-      }
+      if (kd < NB && pending) wait_cols();  // the prefetch just issued overlaps the next panel
       // warp 0: next diagonal block; warps 1..7: rest of this step's update
       if (warp == 0) {
-        const int f = potrf_diag(s1, j1, min(NB, n - j1));
+        trace_stamp(step, 3);
+        const int f = (n - j1 >= NB) ? potrf_diag<true>(s1, j1, NB) : potrf_diag<false>(s1, j1, n - j1);
         if (threadIdx.x == 0) s_fail = f;
+        trace_stamp(step, 4);
       } else {
         update_tiles(s0, j0, nb, m, NB / 16, 1 << 20, 1);
+        if (warp == 1) trace_stamp(step, 5);
       }
       __syncthreads();
+      if (threadIdx.x < 32) trace_stamp(step, 6);
       if (s_fail >= 0) {
-        cp_async_wait_all();
-        __syncthreads();
+        drain();
         return j1 + s_fail;
       }
       j0 = j1;
       s0 = s1;
     }
-    cp_async_wait_all();
-    __syncthreads();
+    drain();
     return -1;
   }
 
+  // finish every async copy of this matrix (loads landed, write-backs complete)
+  __device__ void drain() {
+    if (pending) wait_cols();
+    if (threadIdx.x == 0) {
+      bulk_wait0();
+      fence_async_global();
+    }
+    __syncthreads();
+  }
+
   // Backward sweep L^T x = y (y in rhs / bw after the fused forward sweep).  The L
-  // columns stream back from global memory into the (now free) ring in blocks of NB,
-  // kDepth blocks in flight.
+  // columns stream back from HBM into the (now free) ring in blocks of NB with bulk
+  // copies, kDepth blocks in flight (one mbarrier per buffer); the block's y entries
+  // come along with cp.async.
   __device__ void backward() {
     const int n = g.n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kDepth = 4;
     const int nbuf = g.nslot / NB;  // >= kDepth + 1 (host guarantees nslot >= (kDepth+1)*NB)
     const int nblk = (n + NB - 1) / NB;
-    auto buf_of = [&](int b) -> double* { return win + (size_t)(b % nbuf) * NB * g.lds; };
     auto issue = [&](int b) {
       if (b >= 0) {
+        const int k = b % nbuf;
         const int c0 = b * NB;
         const int cols = min(NB, n - c0);
-        const int per = g.kd + 1;
-        double* dst = buf_of(b);
-        for (int idx = threadIdx.x; idx < cols * per; idx += kCtaThreads) {
-          const int c = idx / per, o = idx - c * per;
-          if (o < col_len(c0 + c)) cp_async8(dst + c * g.lds + o, ab + (int64_t)(c0 + c) * g.ldab + o);
+        Piece p{c0, cols, k * NB};
+        int b0, bc;
+        bulk_range(p, ab, b0, bc);
+        for (int c = 0; c < cols; ++c)
+          if (c < b0 || c >= b0 + bc) elem_copy_col(c0 + c, k * NB + c, true);
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(bars + 1 + k, (unsigned)bc * g.ldab * sizeof(double));
+          if (bc > 0)
+            bulk_g2s(win + (size_t)(k * NB + b0) * g.lds, ab + (int64_t)(c0 + b0) * g.ldab,
+                     (unsigned)bc * g.ldab * sizeof(double), bars + 1 + k);
         }
+        if (threadIdx.x < cols) cp_async8(yb + k * NB + threadIdx.x, rhs + c0 + threadIdx.x);
       }
       cp_async_commit();  // always commit (possibly empty) so group counting stays uniform
     };
     for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d);
     for (int b = nblk - 1; b >= 0; --b) {
+      const int k = b % nbuf;
       cp_async_wait_group<kDepth - 1>();
+      mbar_wait(bars + 1 + k, bphase[k]);
       __syncthreads();
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
-      const double* blk = buf_of(b);
+      const double* blk = win + (size_t)k * NB * g.lds;
       const int sx = (c0 + nb) % g.nslot;  // slot of row c0+nb in the x ring
       for (int c = warp; c < nb; c += kCtaWarps) {
         const int j = c0 + c;
@@ -374,7 +601,7 @@ struct CtaBand {
         }
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) s += __shfl_xor_sync(kFull, s, sh);
-        if (lane == 0) Dinv[c] = rhs[j] - s;  // Dinv reused as the block's right-hand side
+        if (lane == 0) Dinv[c] = yb[k * NB + c] - s;  // Dinv reused as the block's right-hand side
       }
       __syncthreads();
       if (warp == 0) {
@@ -392,6 +619,7 @@ struct CtaBand {
           bw[(c0 + lane) % g.nslot] = v;
           rhs[c0 + lane] = v;
         }
+        if (lane == 0) bphase[k] ^= 1u;
       }
       __syncthreads();
       issue(b - kDepth);

@@ -101,27 +101,6 @@ __device__ __forceinline__ void cta_publish(int* flag, int value) {
   }
 }
 
-// ---- optional trace (bcg_set_trace): pivot phase stamps, %globaltimer ns ----------
-// layout: [0] = number of steps recorded; then kTracePhases stamps per step;
-// worker busy/wait ns per CTA after the step records (see bcg_set_trace).
-constexpr int kTracePhases = 8;
-__device__ unsigned long long* g_trace = nullptr;
-__device__ unsigned long long g_trace_cap = 0;
-
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ void trace_stamp(int j, int phase) {
-  unsigned long long* tr = g_trace;
-  if (tr && threadIdx.x == 0) {
-    const unsigned long long idx = 1 + (unsigned long long)j * kTracePhases + phase;
-    if (idx < g_trace_cap) tr[idx] = gtime();
-    if (phase == 0 && (unsigned long long)j + 1 > tr[0]) tr[0] = j + 1;
-  }
-}
-
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -284,14 +263,15 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
     double* f0 = buf[3];
     double* f1 = buf[4];
     double* f2 = buf[5];
+    unsigned long long* tr = g_trace;
     load_tile<NB>(sD, ab, g, 0, 0);
     __syncthreads();
     int fail_col = -1;
     for (int j = 0; j < nblk; ++j) {
       const int nvalid = min(NB, g.n - j * NB);
-      trace_stamp(j, 0);
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 0);
       const int f = potrf_inv_tile<NB>(sD, sX, nvalid);
-      trace_stamp(j, 1);
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 1);
       if (f >= 0) {
         fail_col = j * NB + f;
         if (threadIdx.x == 0) atomicExch(ws.ctrl + 1, fail_col + 1);
@@ -305,7 +285,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         st_release(LR(j, 0), 1);
         st_release(ws.irdy + j, 1);
       }
-      trace_stamp(j, 2);
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 2);
       if (j + 1 >= nblk) break;
       // --- critical near-diagonal work for step j+1 ---
       double* sW = f0;   // L(j+1, j-1), then L(j+1, j)
@@ -321,22 +301,22 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       }
       __syncthreads();
       if (!s_ok) break;
-      trace_stamp(j, 3);
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 3);
       load_tile<NB>(sP, ab, g, j + 1, j);
       load_tile<NB>(sD2, ab, g, j + 1, j + 1);
       if (has_w) load_tile<NB>(sW, ab, g, j + 1, j - 1);
       __syncthreads();
-      trace_stamp(j, 4);
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 4);
       if (has_w) {
         tile_gemm<NB, true>(sP, sW, sLp);   // A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T
         tile_gemm<NB, true>(sD2, sW, sW);   // A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
       }
       tile_gemm<NB, false>(sW, sP, sX);     // L(j+1,j) = A(j+1,j) Linv(j)^T
       tile_gemm<NB, true>(sD2, sW, sW);     // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T
-      trace_stamp(j, 5);
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 5);
       store_tile<NB>(sW, ab, g, j + 1, j);
       cta_publish(LR(j + 1, 1), 1);
-      trace_stamp(j, 6);
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 6);
       // rotate: D <- D2, Lp <- W; free = old D, old Lp, P
       double* oldD = sD;
       double* oldLp = sLp;

@@ -23,8 +23,19 @@ __global__ void __launch_bounds__(kCtaThreads, 2)
 pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int batch, CtaGeom g,
                  int32_t* info) {
   extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) unsigned long long bars[1 + 16];
+  __shared__ unsigned bphase[16];
+  if (threadIdx.x < 17) mbar_init(&bars[threadIdx.x], 1);
+  if (threadIdx.x < 16) bphase[threadIdx.x] = 0;
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  unsigned phase = 0;
   for (int mat = blockIdx.x; mat < batch; mat += gridDim.x) {
     CtaBand<NB, kSolve> w{g};
+    w.bars = bars;
+    w.bphase = bphase;
+    w.phase = phase;
+    w.tr = (blockIdx.x == 0 && mat == 0) ? g_trace : nullptr;
     w.ab = ab0 + (int64_t)mat * stride_ab;
     w.rhs = kSolve ? b0 + (int64_t)mat * stride_b : nullptr;
     double* p = smem;
@@ -34,7 +45,10 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, i
     w.Dinv = p; p += NB;
     w.lbuf = p; p += 32;
     w.bw = kSolve ? p : nullptr;
+    if (kSolve) p += g.nslot;
+    w.yb = kSolve ? p : nullptr;
     const int fail = w.factor();
+    phase = w.phase;
     if (kSolve && fail < 0) w.backward();
     if (threadIdx.x == 0) info[mat] = fail < 0 ? 0 : fail + 1;
     __syncthreads();
@@ -117,7 +131,7 @@ bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb) {
   g.n = n;
   g.kd = kd;
   g.ldab = ldab;
-  g.lds = (kd + 1) | 1;  // odd column stride
+  g.lds = ldab;  // ring slots mirror the global columns (bulk copies move whole columns)
   int ns = kd + nb;
   if (ns & 1) ++ns;
   g.nslot = ns;

@@ -119,14 +119,49 @@ def trace(tag):
     d = np.diff(st[:, :7], axis=1)  # phase durations 0->1 .. 5->6
     nxt = st[1:, 0] - st[:-1, 6]     # gap to next step start
     names = ["potrf_inv", "store_publish", "wait", "load", "gemm", "publish_next"]
-    out = {"config": tag, "steps": steps, "total_ms": float((st[-1, 1] - st[0, 0]) / 1e6)}
+    out = {"config": tag, "steps": steps, "unit": "cycles", "total_cycles": float(st[-1, 1] - st[0, 0])}
     for i, nm in enumerate(names):
         v = d[:-1, i]
-        out[nm + "_us"] = float(np.median(v) / 1e3)
-    out["gap_us"] = float(np.median(nxt) / 1e3)
+        out[nm] = float(np.median(v))
+    out["gap"] = float(np.median(nxt))
     print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace":
     for tg in sys.argv[2:] or ["C2", "C3", "C4"]:
         trace(tg)
+
+
+def trace_cta(tag, batch=1):
+    """Phase breakdown of the one-CTA kernel (block 0, matrix 0)."""
+    from paper_2305_04635_b200 import _lib
+    cfg = CONFIGS[tag]
+    n, k = cfg.dim, cfg.bandwidth
+    a = np.stack([generate_spd(n, k, s).data for s in range(min(batch, 8))])
+    a = np.concatenate([a] * ((batch + 7) // 8))[:batch]
+    a0 = torch.from_numpy(a).cuda()
+    buf = torch.zeros(1 + 8 * (n // 16 + 2), dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    w = a0.clone()
+    bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
+    torch.cuda.synchronize()
+    lib.bcg_set_trace(buf.data_ptr(), buf.numel() * 8)
+    w = a0.clone()
+    bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
+    torch.cuda.synchronize()
+    lib.bcg_set_trace(None, 0)
+    t = buf.cpu().numpy()
+    steps = int(t[0])
+    st = t[1:1 + 8 * steps].reshape(steps, 8).astype(np.float64)[:-2]
+    med = lambda a, b: float(np.median(st[:, b] - st[:, a]))  # noqa: E731  (SM cycles)
+    out = {"config": tag, "batch": batch, "steps": steps, "unit": "cycles",
+           "trsm": med(0, 7), "wait": med(7, 1), "store_part1": med(1, 2),
+           "potrf": med(3, 4), "rest_update": med(2, 5), "lookahead_total": med(2, 6),
+           "step": float(np.median(np.diff(st[:, 0])))}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_cta":
+    trace_cta("C1", 1)
+    trace_cta("C5", 1)
+    trace_cta("C5", 296)
