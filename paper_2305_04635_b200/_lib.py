@@ -13,7 +13,7 @@ import os
 from .errors import BandCholError, DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbandchol_b200.so")
+LIB_PATH = os.environ.get("BCG_LIB") or os.path.join(_HERE, "libbandchol_b200.so")
 
 # (name, restype, argtypes) -- must match include/bandchol_b200.h
 _i64, _i32p, _dp, _vp, _sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t

@@ -159,7 +159,12 @@ struct CtaBand {
   unsigned long long* tr = nullptr;  // trace buffer (block 0 only), see bcg_set_trace
 
   __device__ __forceinline__ void trace_stamp(int j, int ph) const {
+#ifdef BCG_TRACE
     if (tr && (threadIdx.x & 31) == 0) trace_stamp_to(tr, j, ph);
+#else
+    (void)j;
+    (void)ph;
+#endif
   }
 
   // ---- ring addressing: slot(j) = j mod nslot without a division on hot paths ----
@@ -409,54 +414,58 @@ struct CtaBand {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp < w_lo || (w_lo == 1 && warp == 4)) return;
     const int wid = (w_lo == 1) ? (warp < 4 ? warp - 1 : warp - 2) : warp;  // rank among the workers
+    const int nw = (w_lo == 1) ? kCtaWarps - 2 : kCtaWarps;
     const int gr = lane >> 2, gc = lane & 3;
     const int base = j0 + nb;
     const int T = (m + 15) >> 4;
     tj_hi = min(tj_hi, T);
-    if (tj_lo >= tj_hi) return;
-    // tiles of columns [tj_lo, tj_hi): column tj holds T - tj tiles
-    const int first = tj_lo * T - tj_lo * (tj_lo - 1) / 2;
-    const int last = tj_hi * T - tj_hi * (tj_hi - 1) / 2;
-    const int nw = (w_lo == 1) ? kCtaWarps - 2 : kCtaWarps;
-    for (int t = first + wid; t < last; t += nw) {
-      int tj = tj_lo;
-      while (tj + 1 < tj_hi && (tj + 1) * T - (tj + 1) * tj / 2 <= t) ++tj;
-      const int ti = tj + (t - (tj * T - tj * (tj - 1) / 2));
-      const int i0 = ti * 16, q0 = tj * 16;
-      double acc[2][2][2];
-      int ofs[2][2][2];
-      bool ok[2][2][2];
+    int idx = 0;
+    for (int tj = tj_lo; tj < tj_hi; ++tj) {
+      // this lane's 4 columns of the tile column, as window offsets minus the row
+      int cb[2][2];
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int v = 0; v < 2; ++v)
 #pragma unroll
-        for (int v = 0; v < 2; ++v)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
-            ok[u][v][e] = (i < m) && (q <= i);
-            ofs[u][v][e] = slot_from(s0, j0, base + (q < m ? q : 0)) * g.lds + (i - q);
-            acc[u][v][e] = ok[u][v][e] ? win[ofs[u][v][e]] : 0.0;
-          }
-#pragma unroll
-      for (int k0 = 0; k0 < NB; k0 += 4) {
-        const double* pk = P + (k0 + gc) * g.pld;
-        double a[2], b[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) a[u] = -pk[i0 + u * 8 + gr];
-#pragma unroll
-        for (int v = 0; v < 2; ++v) b[v] = pk[q0 + v * 8 + gr];
+        for (int e = 0; e < 2; ++e) {
+          const int q = tj * 16 + v * 8 + 2 * gc + e;
+          cb[v][e] = slot_from(s0, j0, base + (q < m ? q : 0)) * g.lds - q;
+        }
+      for (int ti = tj; ti < T; ++ti, ++idx) {
+        if (idx % nw != wid) continue;
+        const int i0 = ti * 16, q0 = tj * 16;
+        double acc[2][2][2];
+        bool ok[2][2][2];
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int v = 0; v < 2; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], b[v]);
+          for (int v = 0; v < 2; ++v)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
+              ok[u][v][e] = (i < m) && (q <= i);
+              acc[u][v][e] = ok[u][v][e] ? win[cb[v][e] + i] : 0.0;
+            }
+#pragma unroll
+        for (int k0 = 0; k0 < NB; k0 += 4) {
+          const double* pk = P + (k0 + gc) * g.pld;
+          double a[2], b[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) a[u] = -pk[i0 + u * 8 + gr];
+#pragma unroll
+          for (int v = 0; v < 2; ++v) b[v] = pk[q0 + v * 8 + gr];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], b[v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (ok[u][v][e]) win[cb[v][e] + i0 + u * 8 + gr] = acc[u][v][e];
       }
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int v = 0; v < 2; ++v)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            if (ok[u][v][e]) win[ofs[u][v][e]] = acc[u][v][e];
     }
   }
 
@@ -560,7 +569,17 @@ struct CtaBand {
     const int nbuf = g.nslot / NB;  // >= kDepth + 1 (host guarantees nslot >= (kDepth+1)*NB)
     const int nblk = (n + NB - 1) / NB;
     auto issue = [&](int b) {
-      if (b >= 0) {
+      if (b >= 0 && fast) {
+        const int k = b % nbuf;
+        const int c0 = b * NB;
+        const int cols = min(NB, n - c0);
+        if (threadIdx.x == 0) {
+          const unsigned bytes = (unsigned)cols * g.ldab * sizeof(double);
+          mbar_expect_tx(bars + 1 + k, bytes);
+          bulk_g2s(win + (size_t)(k * NB) * g.lds, ab + (int64_t)c0 * g.ldab, bytes, bars + 1 + k);
+        }
+        if (threadIdx.x < cols) cp_async8(yb + k * NB + threadIdx.x, rhs + c0 + threadIdx.x);
+      } else if (b >= 0) {
         const int k = b % nbuf;
         const int c0 = b * NB;
         const int cols = min(NB, n - c0);
@@ -580,11 +599,14 @@ struct CtaBand {
       cp_async_commit();  // always commit (possibly empty) so group counting stays uniform
     };
     for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d);
+    const int tb = nblk + 1;  // trace rows after the factorization's
     for (int b = nblk - 1; b >= 0; --b) {
       const int k = b % nbuf;
+      if (threadIdx.x < 32) trace_stamp(tb + b, 0);
       cp_async_wait_group<kDepth - 1>();
       mbar_wait(bars + 1 + k, bphase[k]);
       __syncthreads();
+      if (threadIdx.x < 32) trace_stamp(tb + b, 1);
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
       const double* blk = win + (size_t)k * NB * g.lds;
@@ -604,6 +626,7 @@ struct CtaBand {
         if (lane == 0) Dinv[c] = yb[k * NB + c] - s;  // Dinv reused as the block's right-hand side
       }
       __syncthreads();
+      if (threadIdx.x < 32) trace_stamp(tb + b, 2);
       if (warp == 0) {
         double v = lane < nb ? Dinv[lane] : 0.0;
         const double dinv = lane < nb ? 1.0 / blk[lane * g.lds] : 0.0;
@@ -622,7 +645,9 @@ struct CtaBand {
         if (lane == 0) bphase[k] ^= 1u;
       }
       __syncthreads();
+      if (threadIdx.x < 32) trace_stamp(tb + b, 3);
       issue(b - kDepth);
+      if (threadIdx.x < 32) trace_stamp(tb + b, 4);
     }
     cp_async_wait_all();
     __syncthreads();

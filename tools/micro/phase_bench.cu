@@ -34,7 +34,22 @@ __global__ void __launch_bounds__(256, 2) k(double* out, long long* cyc, int rep
     if (which == 1) w.update_tiles(0, 0, NB, 100, 0, NB / 16, 0);
     if (which == 2) w.update_tiles(0, 0, NB, 100, NB / 16, 1 << 20, 1);
     if (which == 3) w.update_tiles(0, 0, NB, 100, 0, 1 << 20, 0);
-    if (which >= 4) {
+    if (which == 7) {
+      // the kernel's per-step code mix: TRSM, part-1 update, then POTRF || rest update
+      w.trsm_panel(0, 0, NB, 100);
+      __syncthreads();
+      w.update_tiles(0, 0, NB, 100, 0, NB / 16, 0);
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        long long a0 = clock64();
+        w.template potrf_diag<true>(0, 0, NB);
+        long long a1 = clock64();
+        if (threadIdx.x == 0) tot += a1 - a0;
+      } else {
+        w.update_tiles(0, 0, NB, 100, NB / 16, 1 << 20, 1);
+      }
+    }
+    if (which >= 4 && which < 7) {
       // POTRF timed alone on warp 0 while the other warps do: 4 = nothing, 5 = DMMA updates,
       // 6 = DFMA register work
       if (threadIdx.x < 32) {
@@ -53,6 +68,10 @@ __global__ void __launch_bounds__(256, 2) k(double* out, long long* cyc, int rep
     __syncthreads();
     long long t1 = clock64();
     if (which < 4) tot += t1 - t0;
+    if (which == 7) {  // restore an SPD window for the next round
+      for (int i = threadIdx.x; i < 116 * 101; i += 256) sm[i] = (i % 101 == 0) ? 200.0 : 0.01 * ((i * 7) % 13);
+      __syncthreads();
+    }
   }
   if (threadIdx.x == 0) { cyc[0] = tot / reps; out[0] = sm[5]; }
 }
@@ -67,8 +86,8 @@ int main() {
   size_t sm = (116 * 101 + 16 * 116) * 8;
   cudaFuncSetAttribute(k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const char* names[] = {"trsm", "update_part1", "update_rest_6warps", "update_all_8warps",
-                         "potrf_alone", "potrf_with_dmma", "potrf_with_dfma"};
-  for (int wh = 0; wh < 7; ++wh) {
+                         "potrf_alone", "potrf_with_dmma", "potrf_with_dfma", "potrf_in_step_mix"};
+  for (int wh = 0; wh < 8; ++wh) {
     k<16><<<1, 256, sm>>>(out, cyc, 20, wh); cudaDeviceSynchronize();
     k<16><<<1, 256, sm>>>(out, cyc, 20, wh); cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf("{\"%s_cycles\": %lld, \"err\": \"%s\"}\n", names[wh], h, cudaGetErrorString(cudaGetLastError()));

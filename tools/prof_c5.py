@@ -15,9 +15,13 @@ n, k = 4096, 100
 a = np.stack([generate_spd(n, k, s).data for s in range(8)])
 a = np.concatenate([a] * ((batch + 7) // 8))[:batch]
 a0 = torch.from_numpy(a).cuda()
+solve = len(sys.argv) > 3 and sys.argv[3] == "solve"
+b0 = torch.from_numpy(np.stack([np.linspace(-1, 1, n)] * batch)).cuda()
 for _ in range(reps):
     w = a0.clone()
-    info = bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
+    wb = b0.clone()
+    info = (bc.dpbsv_batched_device(w, n, k, k + 1, wb, batch) if solve
+            else bc.dpbtrf_batched_device(w, n, k, k + 1, batch))
     torch.cuda.synchronize()
     assert int(info.abs().sum().item()) == 0
 print("ok")
