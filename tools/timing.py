@@ -116,9 +116,9 @@ def trace(tag):
     t = buf.cpu().numpy()
     steps = int(t[0])
     st = t[1:1 + 8 * steps].reshape(steps, 8).astype(np.float64)
-    d = np.diff(st[:, :7], axis=1)  # phase durations 0->1 .. 5->6
-    nxt = st[1:, 0] - st[:-1, 6]     # gap to next step start
-    names = ["potrf_inv", "store_publish", "wait", "load", "gemm", "publish_next"]
+    d = np.diff(st[:, :6], axis=1)  # phase durations 0->1 .. 4->5
+    nxt = st[1:, 0] - st[:-1, 5]     # gap to next step start
+    names = ["potrf_and_loads", "publish_L", "lookback_gemms", "trsm", "syrk_publish"]
     out = {"config": tag, "steps": steps, "unit": "cycles", "total_cycles": float(st[-1, 1] - st[0, 0])}
     for i, nm in enumerate(names):
         v = d[:-1, i]
