@@ -263,8 +263,8 @@ __device__ __forceinline__ void trsm_rows(double* sX, const double* __restrict__
 }
 
 // ---- the kernel ------------------------------------------------------------------------
-template <int NB>
-__global__ void __launch_bounds__(kMultiThreads, 2)
+template <int NB, int kPerSM>
+__global__ void __launch_bounds__(kMultiThreads, kPerSM)
 band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* info) {
   static_assert(NB == 32, "the pivot chain is a 32-lane warp POTRF");
   extern __shared__ __align__(16) double smem[];
@@ -445,12 +445,15 @@ inline size_t multi_workspace_bytes(int n, int kd) {
   return multi_flag_bytes(g.nblk, g.T);
 }
 
-inline int launch_multi(double* ab, int n, int kd, int ldab, int32_t* info, void* workspace, int sms,
-                        cudaStream_t st, char* err, size_t errlen) {
+// Occupancy: wide bands (many worker tasks per step) run 3 CTAs per SM for latency
+// hiding; narrower bands keep 2 so the pivot CTA gets the registers of its chain.
+template <int kPerSM>
+inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, void* workspace, int sms,
+                          cudaStream_t st, char* err, size_t errlen) {
   constexpr int NB = kMultiNB;
   MultiGeom g = multi_geom(n, kd, ldab);
   const size_t smem = 5 * (size_t)MultiTile<NB>::ELEMS * sizeof(double);
-  auto k = band_multi_kernel<NB>;
+  auto k = band_multi_kernel<NB, kPerSM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaFuncSetAttribute(band_multi): %s", cudaGetErrorString(e));
@@ -462,7 +465,7 @@ inline int launch_multi(double* ab, int n, int kd, int ldab, int32_t* info, void
     snprintf(err, errlen, "band_multi kernel does not fit on an SM");
     return (int)cudaErrorInvalidConfiguration;
   }
-  if (per_sm > 2) per_sm = 2;
+  if (per_sm > kPerSM) per_sm = kPerSM;
   e = cudaMemsetAsync(workspace, 0, multi_flag_bytes(g.nblk, g.T), st);
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaMemsetAsync(workspace): %s", cudaGetErrorString(e));
@@ -477,6 +480,12 @@ inline int launch_multi(double* ab, int n, int kd, int ldab, int32_t* info, void
     return (int)e;
   }
   return 0;
+}
+
+inline int launch_multi(double* ab, int n, int kd, int ldab, int32_t* info, void* workspace, int sms,
+                        cudaStream_t st, char* err, size_t errlen) {
+  if (kd >= 1000) return launch_multi_t<3>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
+  return launch_multi_t<2>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
 }
 
 }  // namespace bcg
