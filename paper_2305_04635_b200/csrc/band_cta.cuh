@@ -103,6 +103,11 @@ __device__ __forceinline__ void trace_stamp_to(unsigned long long* tr, int j, in
   }
 }
 
+// Re-broadcast a value the compiler cannot prove warp-uniform (read from shared memory)
+// from lane 0: branches on the result are then known not to split the warp, which keeps
+// ptxas from wrapping every later shuffle / __syncwarp in collective divergence handling.
+__device__ __forceinline__ int warp_uniform(int v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -356,7 +361,13 @@ struct CtaBand {
       // rank-1 update of the rest of the row; entries right of the diagonal become
       // garbage that is never read (only c2 <= r is used or stored)
 #pragma unroll
-      for (int c2 = c + 2; c2 < NB; ++c2) row[c2] = fma(-lrc, lbuf[c2], row[c2]);
+      for (int h = 0; h < NB / 2; ++h) {  // two broadcast values per 128-bit load
+        if (2 * h + 1 >= c + 2) {
+          const double2 l2 = reinterpret_cast<const double2*>(lbuf)[h];
+          if (2 * h >= c + 2) row[2 * h] = fma(-lrc, l2.x, row[2 * h]);
+          row[2 * h + 1] = fma(-lrc, l2.y, row[2 * h + 1]);
+        }
+      }
       __syncwarp();
       p = pn;
       rs = rsn;
@@ -491,20 +502,39 @@ struct CtaBand {
     for (int idx = threadIdx.x; idx < NB * g.pld; idx += kCtaThreads) P[idx] = 0.0;
     load_cols(0, min(n, kd + NB));
     wait_cols();
-    if (warp == 0) {
-      const int f = (n >= NB) ? potrf_diag<true>(0, 0, NB) : potrf_diag<false>(0, 0, n);
-      if (threadIdx.x == 0) s_fail = f;
-    }
-    __syncthreads();
-    if (s_fail >= 0) {
-      drain();
-      return s_fail;
-    }
+    // Loop rotated so that one call site factors every diagonal block: iteration k
+    // runs [warp 0: POTRF(k) || warps 1-7: rest of update(k-1)], then TRSM(k), the
+    // write-back of panel k, the part of update(k) that feeds POTRF(k+1), and the
+    // prefetch of the columns step k+1 brings into the window.
+    int jp = -NB, sp = 0, nbp = 0, mp = 0;  // previous step
     int j0 = 0, s0 = 0;
     for (;;) {
       const int nb = min(NB, n - j0);
-      const int m = min(kd, n - j0 - nb);
       const int step = j0 / NB;
+      if (kd < NB && pending) wait_cols();  // the last prefetch overlaps this panel
+      // warp_uniform(): tell ptxas the branch cannot split a warp, so the POTRF's
+      // shuffles compile to plain SHFL instead of collective divergence handling
+      if (warp_uniform(warp) == 0) {
+        trace_stamp(step, 3);
+        const int f = potrf_diag<false>(s0, j0, nb);
+        if (threadIdx.x == 0) s_fail = f;
+        trace_stamp(step, 4);
+      }
+#ifdef BCG_SERIAL_LOOKAHEAD
+      __syncthreads();
+#endif
+      if (warp != 0 && jp >= 0) {
+        update_tiles(sp, jp, nbp, mp, NB / 16, 1 << 20, 1);
+        if (warp == 1) trace_stamp(step, 5);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) trace_stamp(step, 6);
+      const int fl = warp_uniform(s_fail);
+      if (fl >= 0) {
+        drain();
+        return j0 + fl;
+      }
+      const int m = min(kd, n - j0 - nb);
       if (threadIdx.x < 32) trace_stamp(step, 0);
       trsm_panel(s0, j0, nb, m);
       if (threadIdx.x < 32) trace_stamp(step, 7);
@@ -520,29 +550,11 @@ struct CtaBand {
       if (threadIdx.x < 32) trace_stamp(step, 2);
       const int jlo = j0 + NB + kd;
       if (jlo < n) load_cols(jlo, min(n, jlo + NB));
-      const int j1 = j0 + nb;
-      if (j1 >= n) break;
-      int s1 = s0 + nb;
-      if (s1 >= g.nslot) s1 -= g.nslot;
-      if (kd < NB && pending) wait_cols();  // the prefetch just issued overlaps the next panel
-      // warp 0: next diagonal block; warps 1..7: rest of this step's update
-      if (warp == 0) {
-        trace_stamp(step, 3);
-        const int f = (n - j1 >= NB) ? potrf_diag<true>(s1, j1, NB) : potrf_diag<false>(s1, j1, n - j1);
-        if (threadIdx.x == 0) s_fail = f;
-        trace_stamp(step, 4);
-      } else {
-        update_tiles(s0, j0, nb, m, NB / 16, 1 << 20, 1);
-        if (warp == 1) trace_stamp(step, 5);
-      }
-      __syncthreads();
-      if (threadIdx.x < 32) trace_stamp(step, 6);
-      if (s_fail >= 0) {
-        drain();
-        return j1 + s_fail;
-      }
-      j0 = j1;
-      s0 = s1;
+      if (j0 + nb >= n) break;
+      jp = j0; sp = s0; nbp = nb; mp = m;
+      j0 += nb;
+      s0 += nb;
+      if (s0 >= g.nslot) s0 -= g.nslot;
     }
     drain();
     return -1;
@@ -604,7 +616,7 @@ struct CtaBand {
       const int k = b % nbuf;
       if (threadIdx.x < 32) trace_stamp(tb + b, 0);
       cp_async_wait_group<kDepth - 1>();
-      mbar_wait(bars + 1 + k, bphase[k]);
+      mbar_wait(bars + 1 + k, (unsigned)warp_uniform((int)bphase[k]));
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(tb + b, 1);
       const int c0 = b * NB;

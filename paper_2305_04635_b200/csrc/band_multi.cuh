@@ -276,7 +276,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   __shared__ double lbuf[32];
   __shared__ double sdinv[NB];
   const int T = g.T, nblk = g.nblk;
-  const int warp = threadIdx.x >> 5;
+  const int warp = warp_uniform(threadIdx.x >> 5);  // provably warp-uniform branches
   auto TC = [&](int R, int d) -> int* { return ws.tcnt + (size_t)R * (T + 1) + d; };
   auto LR = [&](int R, int d) -> int* { return ws.lrdy + (size_t)R * (T + 1) + d; };
   auto make_dinv = [&](const double* sL) {  // 1/diag for the substitution TRSM
@@ -316,7 +316,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
           s_ok = ok;
         }
         named_sync(1, 224);
-        if (s_ok) {
+        if (warp_uniform(s_ok)) {
           const int t = threadIdx.x - 32;
           load_tile<NB, 224>(sP, ab, g, j + 1, j, t);
           load_tile<NB, 224>(sD2, ab, g, j + 1, j + 1, t);
@@ -325,12 +325,14 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       }
       __syncthreads();
       if (threadIdx.x == 0) trace_stamp_to(tr, j, 1);
-      if (s_fail >= 0) {
-        fail_col = j * NB + s_fail;
+      const int fl = warp_uniform(s_fail);
+      const int okn = warp_uniform(s_ok);
+      if (fl >= 0) {
+        fail_col = j * NB + fl;
         if (threadIdx.x == 0) atomicExch(ws.ctrl + 1, fail_col + 1);
         break;
       }
-      if (next && !s_ok) break;  // aborting
+      if (next && !okn) break;  // aborting
       // ---- stage B: publish L(j,j), finish the next step's near-diagonal tiles ----
       store_tile<NB>(sD, ab, g, j, j);
       cta_publish(LR(j, 0), 1);
@@ -377,7 +379,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(ws.ctrl, 1);
     __syncthreads();
-    const long long t = s_task;
+    const long long t = warp_uniform(s_task);
     if (t >= total) break;
     const int j = (int)(t / Q), q = (int)(t - (long long)j * Q);
     if (q < T - 1) {
@@ -388,7 +390,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         s_ok = spin_ge(LR(j, 0), 1, ws.ctrl + 1, 256) &&
                spin_ge(TC(R, R - j), j - max(0, R - T), ws.ctrl + 1, 256);
       __syncthreads();
-      if (!s_ok) break;
+      if (!warp_uniform(s_ok)) break;
       load_tile<NB, kMultiThreads>(sA, ab, g, R, j, threadIdx.x);
       load_tile<NB, kMultiThreads>(sB, ab, g, j, j, threadIdx.x);
       __syncthreads();
@@ -412,7 +414,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         s_ok = spin_ge(LR(R, R - j), 1, ws.ctrl + 1, 256) && spin_ge(LR(S, S - j), 1, ws.ctrl + 1, 256) &&
                spin_ge(TC(R, R - S), done, ws.ctrl + 1, 256);
       __syncthreads();
-      if (!s_ok) break;
+      if (!warp_uniform(s_ok)) break;
       load_tile<NB, kMultiThreads>(sA, ab, g, R, j, threadIdx.x);
       load_tile<NB, kMultiThreads>(sB, ab, g, S, j, threadIdx.x);
       load_tile<NB, kMultiThreads>(sC, ab, g, R, S, threadIdx.x);

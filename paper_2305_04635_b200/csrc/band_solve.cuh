@@ -35,7 +35,7 @@ __device__ int first_nonpositive_diag(const double* __restrict__ ab, int n, int 
 __device__ void band_forward(const double* __restrict__ ab, int n, int kd, int ldab, double* b) {
   constexpr int NB = kSolveNB;
   __shared__ double red[kCtaThreads / 32][NB];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
   for (int r0 = 0; r0 < n; r0 += NB) {
     const int nb = min(NB, n - r0);
     const int i = r0 + lane;
@@ -76,7 +76,7 @@ __device__ void band_backward(const double* __restrict__ ab, int n, int kd, int 
   constexpr int kWarps = kCtaThreads / 32;
   __shared__ double sv[NB];
   __shared__ double dblk[NB][NB + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
   const int last0 = ((n - 1) / NB) * NB;
   for (int c0 = last0; c0 >= 0; c0 -= NB) {
     const int nb = min(NB, n - c0);

@@ -14,11 +14,9 @@ __global__ void lat_dmma(long long* cyc, double* out) {
 }
 
 template <int NB>
-__global__ void __launch_bounds__(256, 2) k(double* out, long long* cyc, int reps, int which) {
+__global__ void __launch_bounds__(256, 2) k(double* out, long long* cyc, int reps, int which, CtaGeom g, int s0p, int j0p) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ double D[NB * NB], Dinv[NB], lbuf[32];
-  CtaGeom g;
-  g.n = 1 << 20; g.kd = 100; g.ldab = 101; g.lds = 101; g.nslot = 116; g.pld = 116;
+  __shared__ __align__(16) double D[NB * NB], Dinv[NB], lbuf[32];
   CtaBand<NB, false> w{g};
   w.ab = nullptr; w.rhs = nullptr; w.win = sm; w.P = sm + 116 * 101; w.D = D; w.Dinv = Dinv; w.lbuf = lbuf;
   for (int i = threadIdx.x; i < 116 * 101; i += 256) sm[i] = (i % 101 == 0) ? 200.0 : 0.01 * ((i * 7) % 13);
@@ -54,7 +52,7 @@ __global__ void __launch_bounds__(256, 2) k(double* out, long long* cyc, int rep
       // 6 = DFMA register work
       if (threadIdx.x < 32) {
         long long a0 = clock64();
-        w.template potrf_diag<true>(0, 0, NB);
+        w.template potrf_diag<false>(s0p, j0p, NB);
         long long a1 = clock64();
         if (threadIdx.x == 0) tot += a1 - a0;
       } else if (which == 5 && (threadIdx.x >> 5) != 4) {
@@ -87,9 +85,11 @@ int main() {
   cudaFuncSetAttribute(k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const char* names[] = {"trsm", "update_part1", "update_rest_6warps", "update_all_8warps",
                          "potrf_alone", "potrf_with_dmma", "potrf_with_dfma", "potrf_in_step_mix"};
+  CtaGeom g;
+  g.n = 1 << 20; g.kd = 100; g.ldab = 101; g.lds = 101; g.nslot = 116; g.pld = 116;
   for (int wh = 0; wh < 8; ++wh) {
-    k<16><<<1, 256, sm>>>(out, cyc, 20, wh); cudaDeviceSynchronize();
-    k<16><<<1, 256, sm>>>(out, cyc, 20, wh); cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    k<16><<<1, 256, sm>>>(out, cyc, 20, wh, g, 5, 16*37); cudaDeviceSynchronize();
+    k<16><<<1, 256, sm>>>(out, cyc, 20, wh, g, 5, 16*37); cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf("{\"%s_cycles\": %lld, \"err\": \"%s\"}\n", names[wh], h, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
