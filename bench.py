@@ -34,6 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_2305_04635_b200.inputs import CONFIGS, generate_spd, generate_spd_wide, make_rhs  # noqa: E402
+from paper_2305_04635_b200.sharding import shard  # noqa: E402
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
@@ -127,13 +128,6 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
-
-
-def shard(batch: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous partition of the batch: rank r gets [lo, hi)."""
-    lo = (batch * rank) // world
-    hi = (batch * (rank + 1)) // world
-    return lo, hi
 
 
 def measured_hbm_gbs() -> tuple[float, str]:

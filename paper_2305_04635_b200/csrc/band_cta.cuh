@@ -570,98 +570,143 @@ struct CtaBand {
     __syncthreads();
   }
 
-  // Backward sweep L^T x = y (y in rhs / bw after the fused forward sweep).  The L
-  // columns stream back from HBM into the (now free) ring in blocks of NB with bulk
-  // copies, kDepth blocks in flight (one mbarrier per buffer); the block's y entries
-  // come along with cp.async.
+  // Backward sweep L^T x = y (y in rhs after the fused forward sweep).
+  //
+  // Block b = columns [b*NB, b*NB+nb): s_j = y_j - sum_{i >= b*NB+nb} L(i,j) x_i, then the
+  // upper-triangular solve L11^T x_b = s.  The sum splits into a "far" part (x of blocks
+  // >= b+2, known one block early) and a "near" part (x of block b+1).  Iteration b runs
+  //   warp 0:     near(b) (16x16 GEMV) + triangular solve(b) with L11 in registers
+  //   warps 1-7:  far(b-1) for the next block, concurrently
+  // so the per-block critical path is the 16-step shuffle chain only.  L blocks (and the y
+  // entries) stream in with bulk copies, kDepth blocks ahead, one mbarrier per ring buffer.
   __device__ void backward() {
     const int n = g.n;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
     constexpr int kDepth = 4;
     const int nbuf = g.nslot / NB;  // >= kDepth + 1 (host guarantees nslot >= (kDepth+1)*NB)
     const int nblk = (n + NB - 1) / NB;
+    double* sfar = Dinv;            // 2 x NB: far part (incl. y) per block, double-buffered
+    const bool bulk_y = fast && !(((uintptr_t)rhs) & 15);
+    // usage parity of buffer k's mbarrier for block b (blocks visit buffers in decreasing order)
+    auto parity = [&](int b) -> unsigned {
+      const int k = b % nbuf;
+      int first = nblk - 1 - ((nblk - 1 - k) % nbuf + nbuf) % nbuf;  // largest block on buffer k
+      return (bphase[k] + (unsigned)((first - b) / nbuf)) & 1u;
+    };
     auto issue = [&](int b) {
-      if (b >= 0 && fast) {
-        const int k = b % nbuf;
-        const int c0 = b * NB;
-        const int cols = min(NB, n - c0);
+      if (b < 0) return;
+      const int k = b % nbuf;
+      const int c0 = b * NB;
+      const int cols = min(NB, n - c0);
+      if (fast) {
         if (threadIdx.x == 0) {
           const unsigned bytes = (unsigned)cols * g.ldab * sizeof(double);
-          mbar_expect_tx(bars + 1 + k, bytes);
+          const unsigned ybytes = (bulk_y && cols % 2 == 0) ? cols * sizeof(double) : 0;
+          mbar_expect_tx(bars + 1 + k, bytes + ybytes);
           bulk_g2s(win + (size_t)(k * NB) * g.lds, ab + (int64_t)c0 * g.ldab, bytes, bars + 1 + k);
+          if (ybytes) bulk_g2s(yb + k * NB, rhs + c0, ybytes, bars + 1 + k);
+          else for (int t = 0; t < cols; ++t) yb[k * NB + t] = rhs[c0 + t];
         }
-        if (threadIdx.x < cols) cp_async8(yb + k * NB + threadIdx.x, rhs + c0 + threadIdx.x);
-      } else if (b >= 0) {
-        const int k = b % nbuf;
-        const int c0 = b * NB;
-        const int cols = min(NB, n - c0);
-        Piece p{c0, cols, k * NB};
-        int b0, bc;
-        bulk_range(p, ab, b0, bc);
-        for (int c = 0; c < cols; ++c)
-          if (c < b0 || c >= b0 + bc) elem_copy_col(c0 + c, k * NB + c, true);
-        if (threadIdx.x == 0) {
-          mbar_expect_tx(bars + 1 + k, (unsigned)bc * g.ldab * sizeof(double));
-          if (bc > 0)
-            bulk_g2s(win + (size_t)(k * NB + b0) * g.lds, ab + (int64_t)(c0 + b0) * g.ldab,
-                     (unsigned)bc * g.ldab * sizeof(double), bars + 1 + k);
+      } else {
+        // element-wise fallback: synchronous copies, visible after the caller's barrier
+        for (int c = 0; c < cols; ++c) {
+          double* sp = win + (size_t)(k * NB + c) * g.lds;
+          const double* gp = ab + (int64_t)(c0 + c) * g.ldab;
+          for (int o = threadIdx.x; o < g.ldab; o += kCtaThreads) sp[o] = gp[o];
         }
-        if (threadIdx.x < cols) cp_async8(yb + k * NB + threadIdx.x, rhs + c0 + threadIdx.x);
+        for (int t = threadIdx.x; t < cols; t += kCtaThreads) yb[k * NB + t] = rhs[c0 + t];
+        if (threadIdx.x == 0) mbar_expect_tx(bars + 1 + k, 0);
       }
-      cp_async_commit();  // always commit (possibly empty) so group counting stays uniform
     };
-    for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d);
-    const int tb = nblk + 1;  // trace rows after the factorization's
-    for (int b = nblk - 1; b >= 0; --b) {
-      const int k = b % nbuf;
-      if (threadIdx.x < 32) trace_stamp(tb + b, 0);
-      cp_async_wait_group<kDepth - 1>();
-      mbar_wait(bars + 1 + k, (unsigned)warp_uniform((int)bphase[k]));
-      __syncthreads();
-      if (threadIdx.x < 32) trace_stamp(tb + b, 1);
+    // far part of block b from x entries of blocks >= b+2 (warps 1-7)
+    auto far = [&](int b) {
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
+      const int k = b % nbuf;
       const double* blk = win + (size_t)k * NB * g.lds;
-      const int sx = (c0 + nb) % g.nslot;  // slot of row c0+nb in the x ring
-      for (int c = warp; c < nb; c += kCtaWarps) {
+      const int rlo = c0 + nb + NB;  // first row of block b+2
+      const int sx = rlo % g.nslot;
+      for (int c = warp - 1; c < nb; c += kCtaWarps - 1) {
         const int j = c0 + c;
         const int len = col_len(j);
         const double* colj = blk + c * g.lds;
-        double s = 0.0;
-        for (int o = nb - c + lane; o < len; o += 32) {
-          int sl = sx + (j + o - (c0 + nb));
+        double acc = 0.0;
+        for (int o = (rlo - j) + lane; o < len; o += 32) {
+          int sl = sx + (j + o - rlo);
           if (sl >= g.nslot) sl -= g.nslot;
-          s = fma(colj[o], bw[sl], s);
+          acc = fma(colj[o], bw[sl], acc);
         }
 #pragma unroll
-        for (int sh = 16; sh > 0; sh >>= 1) s += __shfl_xor_sync(kFull, s, sh);
-        if (lane == 0) Dinv[c] = yb[k * NB + c] - s;  // Dinv reused as the block's right-hand side
+        for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(kFull, acc, sh);
+        if (lane == 0) sfar[(b & 1) * NB + c] = yb[k * NB + c] - acc;
       }
-      __syncthreads();
-      if (threadIdx.x < 32) trace_stamp(tb + b, 2);
+    };
+    for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d);
+    const int tb = nblk + 1;  // trace rows after the factorization's
+    // prologue: far part of the last block (nothing beyond it)
+    mbar_wait(bars + 1 + (nblk - 1) % nbuf, parity(nblk - 1));
+    __syncthreads();
+    if (warp != 0) far(nblk - 1);
+    for (int b = nblk - 1; b >= 0; --b) {
+      const int k = b % nbuf;
+      const int c0 = b * NB;
+      const int nb = min(NB, n - c0);
+      if (threadIdx.x < 32) trace_stamp(tb + b, 0);
+      if (b >= 1) mbar_wait(bars + 1 + (b - 1) % nbuf, parity(b - 1));  // block b-1 for far(b-1)
+      __syncthreads();  // far(b) done, x of block b+1 visible
+      if (threadIdx.x < 32) trace_stamp(tb + b, 1);
       if (warp == 0) {
-        double v = lane < nb ? Dinv[lane] : 0.0;
-        const double dinv = lane < nb ? 1.0 / blk[lane * g.lds] : 0.0;
+        const double* blk = win + (size_t)k * NB * g.lds;
+        const int r = lane;
+        // L11 column r below the diagonal -> registers; near rows of block b+1 as well
+        double lrow[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) lrow[c] = (r < nb && c > r && c < nb) ? blk[r * g.lds + (c - r)] : 0.0;
+        double v = r < nb ? sfar[(b & 1) * NB + r] : 0.0;
+        if (r < nb) {
+          // near part: rows c0+nb .. c0+nb+NB-1 (block b+1), in band for this column
+          const double* colr = blk + r * g.lds;
+          const int len = col_len(c0 + r);
+          const int sx = (c0 + nb) % g.nslot;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int t = 0; t < NB; t += 2) {
+            const int o0 = nb - r + t, o1 = o0 + 1;
+            int s0i = sx + t, s1i = sx + t + 1;
+            if (s0i >= g.nslot) s0i -= g.nslot;
+            if (s1i >= g.nslot) s1i -= g.nslot;
+            if (o0 < len) a0 = fma(colr[o0], bw[s0i], a0);
+            if (o1 < len) a1 = fma(colr[o1], bw[s1i], a1);
+          }
+          v -= a0 + a1;
+        }
+        const double dinv = r < nb ? 1.0 / blk[r * g.lds] : 0.0;
 #pragma unroll
         for (int c = NB - 1; c >= 0; --c) {
           if (c < nb) {
             const double xc = __shfl_sync(kFull, v * dinv, c);
-            if (lane == c) v = xc;
-            else if (lane < c && lane < nb) v = fma(-blk[lane * g.lds + (c - lane)], xc, v);
+            if (r == c) v = xc;
+            else v = fma(-lrow[c], xc, v);  // lrow[c] = 0 for c <= r
           }
         }
-        if (lane < nb) {
-          bw[(c0 + lane) % g.nslot] = v;
-          rhs[c0 + lane] = v;
+        if (r < nb) {
+          bw[(c0 + r) % g.nslot] = v;
+          rhs[c0 + r] = v;
         }
-        if (lane == 0) bphase[k] ^= 1u;
+      } else if (b >= 1) {
+        far(b - 1);
       }
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(tb + b, 3);
-      issue(b - kDepth);
-      if (threadIdx.x < 32) trace_stamp(tb + b, 4);
+      issue(b - kDepth);  // block b's buffer is free now ... and so is b+1's
     }
-    cp_async_wait_all();
+    // buffer mbarrier phases advanced by this matrix: one completion per block
+    __syncthreads();
+    if (threadIdx.x < nbuf) {
+      int cnt = 0;
+      for (int b = threadIdx.x; b < nblk; b += nbuf) ++cnt;
+      bphase[threadIdx.x] = (bphase[threadIdx.x] + (unsigned)cnt) & 1u;
+    }
     __syncthreads();
   }
 };
