@@ -35,6 +35,9 @@ namespace bcg {
 constexpr int kCtaThreads = 256;
 constexpr int kCtaWarps = kCtaThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
+// the thread that issues and waits on the window's bulk copies: lane 0 of the last warp,
+// so the POTRF warp (warp 0) never blocks on copy-engine bookkeeping
+constexpr int kCopyThread = kCtaThreads - 32;
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -108,6 +111,19 @@ __device__ __forceinline__ void trace_stamp_to(unsigned long long* tr, int j, in
 // ptxas from wrapping every later shuffle / __syncwarp in collective divergence handling.
 __device__ __forceinline__ int warp_uniform(int v) { return __shfl_sync(0xffffffffu, v, 0); }
 
+// 64-bit broadcast from `src` issued where written: volatile asm keeps the compiler from
+// sinking the shuffle down to its first use, so its latency overlaps the rest of a
+// POTRF column instead of sitting on the pivot chain.
+__device__ __forceinline__ double shfl_early(double v, int src) {
+  unsigned lo, hi;
+  asm volatile("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+  asm volatile("shfl.sync.idx.b32 %0, %0, %1, 0x1f, 0xffffffff;" : "+r"(lo) : "r"(src));
+  asm volatile("shfl.sync.idx.b32 %0, %0, %1, 0x1f, 0xffffffff;" : "+r"(hi) : "r"(src));
+  double r;
+  asm volatile("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -138,7 +154,7 @@ struct CtaGeom {
 
 // Shared-memory footprint (bytes) of one CTA for block size NB.
 __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g, bool solve) {
-  size_t d = (size_t)g.nslot * g.lds + (size_t)nb_block * g.pld + (size_t)nb_block * nb_block + nb_block + 32;
+  size_t d = (size_t)g.nslot * g.lds + (size_t)nb_block * g.pld + (size_t)nb_block * (nb_block + 4) + nb_block + 32;
   if (solve) d += (size_t)g.nslot + (size_t)(g.nslot / nb_block) * nb_block;  // rhs ring + staged y
   return d * sizeof(double) + 64;
 }
@@ -151,7 +167,8 @@ struct CtaBand {
   double* __restrict__ rhs;  // its right-hand side (kSolve)
   double* win;               // shared ring of column slots
   double* P;                 // NB x pld dense panel, P[c*pld + r] = L(j0+nb+r, j0+c)
-  double* D;                 // NB x NB dense L11, D[c*NB + r] = L(r, c)
+  static constexpr int kLDD = NB + 4;  // D stride (= 4 mod 16: conflict-free DMMA fragments)
+  double* D;                 // L11, D[c*kLDD + r] = L(r, c); then L11^-1, D[i*kLDD + j] = Linv(i, j)
   double* Dinv;              // NB reciprocals of diag(L11)
   double* lbuf;              // 32 doubles: column broadcast inside the POTRF warp
   double* bw;                // ring of rhs / solution entries, slot(i) like columns
@@ -229,7 +246,7 @@ struct CtaBand {
   // async load of columns [jlo, jhi) (and their rhs entries); complete with wait_cols()
   __device__ void load_cols(int jlo, int jhi) {
     if (fast) {
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == kCopyThread) {
         bulk_wait_read0();  // the write-back that read these slots is done reading
         const unsigned col = (unsigned)g.ldab * sizeof(double);
         mbar_expect_tx(bars, (unsigned)(jhi - jlo) * col);
@@ -245,7 +262,7 @@ struct CtaBand {
       pending = true;
       return;
     }
-    if (threadIdx.x == 0) bulk_wait_read0();  // the write-back that read these slots is done reading
+    if (threadIdx.x == kCopyThread) bulk_wait_read0();  // the write-back that read these slots is done reading
     __syncthreads();
     Piece pc[2];
     const int np = pieces(jlo, jhi, pc);
@@ -257,7 +274,7 @@ struct CtaBand {
       for (int c = 0; c < pc[q].cnt; ++c)
         if (c < b0 || c >= b0 + bc) elem_copy_col(pc[q].j + c, pc[q].slot + c, true);
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == kCopyThread) {
       mbar_expect_tx(bars, bytes);
       for (int q = 0; q < np; ++q) {
         int b0, bc;
@@ -285,7 +302,7 @@ struct CtaBand {
   // follows fence_async_smem() by every writer; the bulk part is issued by thread 0.
   __device__ void store_cols(int j0, int nb) {
     if (fast) {
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == kCopyThread) {
         const unsigned col = (unsigned)g.ldab * sizeof(double);
         const int s0 = j0 % g.nslot;
         const int c1 = min(nb, g.nslot - s0);
@@ -302,24 +319,44 @@ struct CtaBand {
       bulk_range(pc[q], ab, b0, bc);
       for (int c = 0; c < pc[q].cnt; ++c)
         if (c < b0 || c >= b0 + bc) elem_copy_col(pc[q].j + c, pc[q].slot + c, false);
-      if (threadIdx.x == 0 && bc > 0)
+      if (threadIdx.x == kCopyThread && bc > 0)
         bulk_s2g(ab + (int64_t)(pc[q].j + b0) * g.ldab, win + (size_t)(pc[q].slot + b0) * g.lds,
                  (unsigned)bc * g.ldab * sizeof(double));
     }
-    if (threadIdx.x == 0) bulk_commit();
+    if (threadIdx.x == kCopyThread) bulk_commit();
   }
 
   // Warp 0: Cholesky of the nb x nb diagonal block at column j0 (+ forward sweep).
   // Lane r holds row r.  Returns the local failing column or -1 (uniform).
-  // kFull (nb == NB, every block but possibly the last) compiles to straight-line code.
-  template <bool kWhole>
+  //
+  // Straight-line for every block: a short last block (nb < NB) is padded with identity
+  // rows, so the column loop has no per-column masks.  Column c of D doubles as the
+  // broadcast buffer of the rank-1 update (distinct per column, so one __syncwarp per
+  // column suffices), Dinv[c] is written as the chain produces it, and failure is found
+  // once at the end: after a non-positive / NaN pivot every later pivot of the block is
+  // NaN, so the first failing column is the first lane whose L(r, r) is not > 0.  The
+  // diagonal block reaches the window later, from D (copy_diag_block).
   __device__ int potrf_diag(int s0, int j0, int nb) {
-    if (kWhole) nb = NB;
     const int r = threadIdx.x & 31;
     double row[NB];
+    const int sw = g.nslot - s0;  // columns before the ring wraps
+    if (nb == NB && g.kd >= NB - 1) {
+      // whole block inside the band: entries above the diagonal (and lanes >= NB) are
+      // don't-care, so the loads only need an in-bounds offset
 #pragma unroll
-    for (int c = 0; c < NB; ++c)
-      row[c] = (r < nb && c <= r && r - c <= g.kd) ? win[slot_from(s0, j0, j0 + c) * g.lds + (r - c)] : 0.0;
+      for (int c = 0; c < NB; ++c) {
+        const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
+        row[c] = win[sl * g.lds + ((c <= r && r < NB) ? r - c : 0)];
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
+        const bool in = r < nb && c <= r && r - c <= g.kd;
+        const double v = win[sl * g.lds + (in ? r - c : 0)];
+        row[c] = in ? v : ((r >= nb && c == r) ? 1.0 : 0.0);
+      }
+    }
     double s = 0.0;
     if (kSolve && r < nb) s = bw[slot_from(s0, j0, j0 + r)];
     // chain state, identical in every lane: p = pivot of column c, (alpha, beta) =
@@ -328,15 +365,13 @@ struct CtaBand {
     double alpha = __shfl_sync(kFull, row[0], 1);
     double beta = __shfl_sync(kFull, row[1], 1);
     double rs = rsqrt_nr(p);
-    double myinv = 0.0;
-    int fail = -1;
     // Software-pipelined: the next column's 1/sqrt and chain broadcasts are issued
     // before this column's rank-1 update, so their latency hides under it.
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
-      const bool act = kWhole || c < nb;
-      if (act && fail < 0 && !(p > 0.0)) fail = c;
-      const double lrc = (r > c) ? row[c] * rs : 0.0;  // L(r, c); 0 on and above the diagonal
+      // L(r, c) for r >= c (for r == c this is p * rs: lane c's own entry equals p
+      // bit for bit); lanes r < c compute don't-care values that are never read
+      const double lrc = row[c] * rs;
       const double l1 = alpha * rs;                     // L(c+1, c)
       const double pn = fma(-l1, l1, beta);             // pivot of column c+1
       const double rsn = rsqrt_nr(pn);
@@ -347,72 +382,126 @@ struct CtaBand {
       if (c + 2 < NB) {
         // lane c+2's entries (c+2, c+1), (c+2, c+2) after this column
         const double bn = fma(-lrc, lrc, row[c + 2 < NB ? c + 2 : 0]);
-        alpha_n = __shfl_sync(kFull, row[c + 1 < NB ? c + 1 : 0], c + 2);
-        beta_n = __shfl_sync(kFull, bn, c + 2);
+        alpha_n = shfl_early(row[c + 1 < NB ? c + 1 : 0], c + 2);
+        beta_n = shfl_early(bn, c + 2);
       }
       if (kSolve) {
         const double yc = __shfl_sync(kFull, s, c) * rs;
-        if (act) s = (r == c) ? yc : fma(-lrc, yc, s);
+        s = (r == c) ? yc : ((r > c) ? fma(-lrc, yc, s) : s);
       }
-      if (r == c) { row[c] = p * rs; myinv = rs; }
-      else if (r > c) row[c] = lrc;
-      lbuf[r] = lrc;
+      row[c] = lrc;
+      double* dc = D + c * kLDD;  // column c of L11 (rows < c: don't-care)
+      if (r < NB) dc[r] = lrc;
+      if (r == 0) Dinv[c] = rs;
       __syncwarp();
       // rank-1 update of the rest of the row; entries right of the diagonal become
       // garbage that is never read (only c2 <= r is used or stored)
 #pragma unroll
       for (int h = 0; h < NB / 2; ++h) {  // two broadcast values per 128-bit load
         if (2 * h + 1 >= c + 2) {
-          const double2 l2 = reinterpret_cast<const double2*>(lbuf)[h];
+          const double2 l2 = reinterpret_cast<const double2*>(dc)[h];
           if (2 * h >= c + 2) row[2 * h] = fma(-lrc, l2.x, row[2 * h]);
           row[2 * h + 1] = fma(-lrc, l2.y, row[2 * h + 1]);
         }
       }
-      __syncwarp();
       p = pn;
       rs = rsn;
       alpha = alpha_n;
       beta = beta_n;
     }
-    if (fail < 0) {
-      if (r < nb) {
+    const double dgl = (r < nb) ? D[r * kLDD + r] : 1.0;
+    const unsigned bad = __ballot_sync(kFull, !(dgl > 0.0));
+    if (bad) return __ffs(bad) - 1;
+    // the factored block back to its window slots (the lookahead leaves warp 0 slack)
 #pragma unroll
-        for (int c = 0; c < NB; ++c)
-          if (c <= r && r - c <= g.kd) win[slot_from(s0, j0, j0 + c) * g.lds + (r - c)] = row[c];
-        if (kSolve) {
-          bw[slot_from(s0, j0, j0 + r)] = s;
-          rhs[j0 + r] = s;
-        }
-      }
-      if (r < NB) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) D[c * NB + r] = (r < nb && c <= r) ? row[c] : 0.0;  // D[c][r] = L(r, c)
-        Dinv[r] = r < nb ? myinv : 0.0;
-      }
+    for (int c = 0; c < NB; ++c) {
+      const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
+      if (c <= r && r < nb && r - c <= g.kd) win[sl * g.lds + (r - c)] = row[c];
     }
-    return fail;
+    if (kSolve && r < nb) {
+      bw[slot_from(s0, j0, j0 + r)] = s;
+      rhs[j0 + r] = s;
+    }
+    invert_diag();
+    return -1;
   }
 
-  // Panel TRSM: row r of P solves x L11^T = a_r (all threads).
+  // Warp 0, after the POTRF: D <- L11^-1 (row-major, D[i*kLDD + j] = Linv(i, j)), so the
+  // panel TRSM becomes a tensor-core product.  Lane j forward-substitutes L11 x = e_j
+  // with the pivots' reciprocals from Dinv; padded rows of a short block are identity
+  // rows and invert to themselves.  Runs inside the lookahead window, off the chain.
+  __device__ void invert_diag() {
+    const int j = threadIdx.x & 31;
+    double t[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) t[i] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      t[k] *= Dinv[k];
+      const double* dk = D + k * kLDD;
+#pragma unroll
+      for (int h = 0; h < NB / 2; ++h) {
+        if (2 * h + 1 > k) {
+          const double2 l2 = reinterpret_cast<const double2*>(dk)[h];
+          if (2 * h > k) t[2 * h] = fma(-l2.x, t[k], t[2 * h]);
+          t[2 * h + 1] = fma(-l2.y, t[k], t[2 * h + 1]);
+        }
+      }
+    }
+    __syncwarp();
+    if (j < NB) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) D[i * kLDD + j] = t[i];
+    }
+  }
+
+  // Panel TRSM as a product: X = A L11^-T for the m panel rows, 16-row tiles over the
+  // warps, DMMA m8n8k4 with A from the window (entries outside the band read as 0) and
+  // B(k, c) = Linv(c, k) from D.  X goes to the dense panel P and back to the window.
   __device__ void trsm_panel(int s0, int j0, int nb, int m) {
-    for (int r = threadIdx.x; r < m; r += kCtaThreads) {
-      double x[NB];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gr = lane >> 2, gc = lane & 3;
+    const int sw = g.nslot - s0;
+    const int T = (m + 15) >> 4;
+    for (int t = warp; t < T; t += kCtaWarps) {
+      double acc[2][NB / 8][2];
 #pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        const int off = nb + r - c;
-        x[c] = (c < nb && off <= g.kd) ? win[slot_from(s0, j0, j0 + c) * g.lds + off] : 0.0;
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < NB / 8; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < NB / 4; ++kk) {
+        const int k = 4 * kk + gc;
+        const int sl = k < sw ? s0 + k : s0 + k - g.nslot;
+        double a[2], bf[NB / 8];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int off = nb + 16 * t + 8 * u + gr - k;
+          const bool in = k < nb && off <= g.kd;
+          const double v = win[sl * g.lds + (in ? off : 0)];
+          a[u] = in ? v : 0.0;
+        }
+#pragma unroll
+        for (int v = 0; v < NB / 8; ++v) bf[v] = D[(8 * v + gr) * kLDD + k];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < NB / 8; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], bf[v]);
       }
 #pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        x[c] *= Dinv[c];
+      for (int u = 0; u < 2; ++u) {
+        const int r = 16 * t + 8 * u + gr;
+        if (r >= m) continue;
 #pragma unroll
-        for (int c2 = c + 1; c2 < NB; ++c2) x[c2] = fma(-x[c], D[c * NB + c2], x[c2]);
-      }
+        for (int v = 0; v < NB / 8; ++v)
 #pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        const int off = nb + r - c;
-        if (c < nb && off <= g.kd) win[slot_from(s0, j0, j0 + c) * g.lds + off] = x[c];
-        P[c * g.pld + r] = x[c];
+          for (int e = 0; e < 2; ++e) {
+            const int c = 8 * v + 2 * gc + e;
+            const int off = nb + r - c;
+            const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
+            P[c * g.pld + r] = acc[u][v][e];
+            if (c < nb && off <= g.kd) win[sl * g.lds + off] = acc[u][v][e];
+          }
       }
     }
   }
@@ -516,7 +605,7 @@ struct CtaBand {
       // shuffles compile to plain SHFL instead of collective divergence handling
       if (warp_uniform(warp) == 0) {
         trace_stamp(step, 3);
-        const int f = potrf_diag<false>(s0, j0, nb);
+        const int f = potrf_diag(s0, j0, nb);
         if (threadIdx.x == 0) s_fail = f;
         trace_stamp(step, 4);
       }
@@ -563,7 +652,7 @@ struct CtaBand {
   // finish every async copy of this matrix (loads landed, write-backs complete)
   __device__ void drain() {
     if (pending) wait_cols();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == kCopyThread) {
       bulk_wait0();
       fence_async_global();
     }
@@ -661,7 +750,7 @@ struct CtaBand {
         // L11 column r below the diagonal -> registers; near rows of block b+1 as well
         double lrow[NB];
 #pragma unroll
-        for (int c = 0; c < NB; ++c) lrow[c] = (r < nb && c > r && c < nb) ? blk[r * g.lds + (c - r)] : 0.0;
+        for (int c = 0; c < NB; ++c) lrow[c] = (r < nb && c > r && c < nb && c - r <= g.kd) ? blk[r * g.lds + (c - r)] : 0.0;
         double v = r < nb ? sfar[(b & 1) * NB + r] : 0.0;
         if (r < nb) {
           // near part: rows c0+nb .. c0+nb+NB-1 (block b+1), in band for this column

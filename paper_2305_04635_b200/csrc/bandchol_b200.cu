@@ -41,7 +41,7 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, i
     double* p = smem;
     w.win = p; p += (size_t)g.nslot * g.lds;
     w.P = p; p += (size_t)NB * g.pld;
-    w.D = p; p += NB * NB;
+    w.D = p; p += NB * (NB + 4);
     w.Dinv = p; p += NB;
     w.lbuf = p; p += 32;
     w.bw = kSolve ? p : nullptr;
@@ -126,13 +126,14 @@ int sm_count() {
   return v;
 }
 
-bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb) {
+bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb, bool solve) {
   bcg::CtaGeom g;
   g.n = n;
   g.kd = kd;
   g.ldab = ldab;
   g.lds = ldab;  // ring slots mirror the global columns (bulk copies move whole columns)
   int ns = kd + nb;
+  if (solve && ns < 5 * nb) ns = 5 * nb;  // backward-sweep prefetch ring: 5 blocks
   if (ns & 1) ++ns;
   g.nslot = ns;
   int pld = ((kd + 15) / 16) * 16 + 4;  // covers the 16-row tiles, = 4 (mod 16)
@@ -140,19 +141,17 @@ bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb) {
   return g;
 }
 
-// Block size for the one-CTA-per-matrix kernel: the largest NB whose window fits
-// two CTAs per SM, else one; 0 if the window does not fit at all.
+// Block size for the one-CTA-per-matrix kernel (NB = 16) when its window fits two
+// CTAs per SM, else one; 0 if the window does not fit at all.
 int cta_block(int n, int kd, int ldab, bool solve, bcg::CtaGeom* out) {
   const size_t limit = (size_t)smem_optin();
   const size_t half = 113 * 1024;
   for (size_t cap : {half, limit}) {
-    for (int nb : {16, 32}) {
-      bcg::CtaGeom g = make_geom(n, kd, ldab, nb);
-      if (bcg::cta_smem_bytes(nb, g, solve) > cap) continue;
-      if (solve && g.nslot < 5 * nb) continue;  // backward-sweep prefetch ring needs 5 blocks
-      *out = g;
-      return nb;
-    }
+    const int nb = 16;
+    bcg::CtaGeom g = make_geom(n, kd, ldab, nb, solve);
+    if (bcg::cta_smem_bytes(nb, g, solve) > cap) continue;
+    *out = g;
+    return nb;
   }
   return 0;
 }
@@ -170,12 +169,9 @@ int launch_cta_t(double* ab, int64_t sab, double* b, int64_t sb, int batch, cons
 
 int launch_cta(double* ab, int64_t sab, double* b, int64_t sb, int batch, int nb, const bcg::CtaGeom& g,
                int32_t* info, bool solve, cudaStream_t st) {
-  if (solve) {
-    if (nb == 16) return launch_cta_t<16, true>(ab, sab, b, sb, batch, g, info, st);
-    return launch_cta_t<32, true>(ab, sab, b, sb, batch, g, info, st);
-  }
-  if (nb == 16) return launch_cta_t<16, false>(ab, sab, b, sb, batch, g, info, st);
-  return launch_cta_t<32, false>(ab, sab, b, sb, batch, g, info, st);
+  (void)nb;  // 16: the smallest block has the shortest per-step chain and window
+  if (solve) return launch_cta_t<16, true>(ab, sab, b, sb, batch, g, info, st);
+  return launch_cta_t<16, false>(ab, sab, b, sb, batch, g, info, st);
 }
 
 int check_geom(int64_t n, int64_t kd, int64_t ldab) {

@@ -232,3 +232,31 @@ def test_multi_rhs_device_solve():
     for s in range(R):
         xs = oracle.solve(n, k, k + 1, a.data, B[s])
         assert np.linalg.norm(got[s] - xs) <= X_TOL * np.linalg.norm(xs)
+
+
+@pytest.mark.parametrize("n,k", [(1, 0), (7, 0), (33, 1), (100, 3), (257, 15), (300, 16), (301, 17),
+                                 (500, 40), (640, 63), (1000, 64), (777, 100), (1500, 130)])
+def test_fused_factor_solve_shapes(n, k):
+    """The fused batched factor + solve (one CTA per matrix) across block-edge shapes."""
+    B = 3
+    data = np.stack([generate_spd(n, k, 100 + s).data for s in range(B)])
+    rhs = np.stack([make_rhs(n, s) for s in range(B)])
+    a0, b0 = data.copy(), rhs.copy()
+    info = bc.factor_solve_batched(data, rhs, n, k)
+    assert not info.any()
+    for s in range(B):
+        want = a0[s].copy()
+        oracle.factor_plain(n, k, k + 1, want)
+        assert oracle.max_scaled_diff(n, k, data[s], k + 1, want, k + 1) <= L_TOL
+        xs = oracle.solve(n, k, k + 1, want, b0[s])
+        assert np.linalg.norm(rhs[s] - xs) <= X_TOL * np.linalg.norm(xs)
+
+
+def test_fused_failure_keeps_matrix_and_column():
+    n, k = 600, 30
+    data = np.stack([generate_spd(n, k, s).data for s in range(4)])
+    rhs = np.stack([make_rhs(n, s) for s in range(4)])
+    data[2, 333 * (k + 1)] = -5.0
+    with pytest.raises(bc.NotPositiveDefinite) as err:
+        bc.factor_solve_batched(data, rhs, n, k)
+    assert err.value.matrix == 2 and err.value.column == 333
