@@ -161,7 +161,7 @@ __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g,
 
 template <int NB, bool kSolve>
 struct CtaBand {
-  static_assert(NB == 16 || NB == 32, "block size");
+  static_assert(NB == 16, "block size: lanes 16-31 of the POTRF warp invert L11");
   const CtaGeom g;
   double* __restrict__ ab;   // this matrix in global memory
   double* __restrict__ rhs;  // its right-hand side (kSolve)
@@ -169,8 +169,8 @@ struct CtaBand {
   double* P;                 // NB x pld dense panel, P[c*pld + r] = L(j0+nb+r, j0+c)
   static constexpr int kLDD = NB + 4;  // D stride (= 4 mod 16: conflict-free DMMA fragments)
   double* D;                 // L11, D[c*kLDD + r] = L(r, c); then L11^-1, D[i*kLDD + j] = Linv(i, j)
-  double* Dinv;              // NB reciprocals of diag(L11)
-  double* lbuf;              // 32 doubles: column broadcast inside the POTRF warp
+  double* Dinv;              // NB doubles of scratch (+ lbuf: the backward sweep's far sums)
+  double* lbuf;              // 32 doubles: sink for the inverse lanes' column stores
   double* bw;                // ring of rhs / solution entries, slot(i) like columns
   double* yb;                // backward sweep: nbuf x NB staged y entries
   unsigned long long* bars;  // mbarriers: [0] window loads, [1 + k] backward buffer k
@@ -178,6 +178,7 @@ struct CtaBand {
   unsigned phase = 0;        // parity of the next wait on bars[0] (uniform register)
   bool pending = false;      // a load_cols is in flight
   bool fast = false;         // every column chunk meets the bulk-copy alignment rules
+  int pw = 0;                // the POTRF warp; warp pw + 4 (same SM sub-partition) idles in the lookahead
   unsigned long long* tr = nullptr;  // trace buffer (block 0 only), see bcg_set_trace
 
   __device__ __forceinline__ void trace_stamp(int j, int ph) const {
@@ -326,27 +327,32 @@ struct CtaBand {
     if (threadIdx.x == kCopyThread) bulk_commit();
   }
 
-  // Warp 0: Cholesky of the nb x nb diagonal block at column j0 (+ forward sweep).
+  // Warp pw: Cholesky of the nb x nb diagonal block at column j0 (+ forward sweep).
   // Lane r holds row r.  Returns the local failing column or -1 (uniform).
   //
   // Straight-line for every block: a short last block (nb < NB) is padded with identity
   // rows, so the column loop has no per-column masks.  Column c of D doubles as the
   // broadcast buffer of the rank-1 update (distinct per column, so one __syncwarp per
-  // column suffices), Dinv[c] is written as the chain produces it, and failure is found
+  // column suffices), lanes NB..31 build L11^-1 along the way, and failure is found
   // once at the end: after a non-positive / NaN pivot every later pivot of the block is
-  // NaN, so the first failing column is the first lane whose L(r, r) is not > 0.  The
-  // diagonal block reaches the window later, from D (copy_diag_block).
+  // NaN, so the first failing column is the first lane whose L(r, r) is not > 0.
   __device__ int potrf_diag(int s0, int j0, int nb) {
     const int r = threadIdx.x & 31;
     double row[NB];
     const int sw = g.nslot - s0;  // columns before the ring wraps
+    // lanes NB..2NB-1 start from e_(r-NB): the column step below is then, for them,
+    // forward substitution L11 x = e_(r-NB), so they finish holding column r-NB of L11^-1
+    // (the panel TRSM is a product with it) at no extra instruction cost
+    const bool inv = r >= NB;
+    const double e = 1.0;
     if (nb == NB && g.kd >= NB - 1) {
-      // whole block inside the band: entries above the diagonal (and lanes >= NB) are
-      // don't-care, so the loads only need an in-bounds offset
+      // whole block inside the band: entries above the diagonal are don't-care, so the
+      // loads only need an in-bounds offset
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
-        row[c] = win[sl * g.lds + ((c <= r && r < NB) ? r - c : 0)];
+        const double v = win[sl * g.lds + ((c <= r && !inv) ? r - c : 0)];
+        row[c] = inv ? (c == r - NB ? e : 0.0) : v;
       }
     } else {
 #pragma unroll
@@ -354,7 +360,7 @@ struct CtaBand {
         const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
         const bool in = r < nb && c <= r && r - c <= g.kd;
         const double v = win[sl * g.lds + (in ? r - c : 0)];
-        row[c] = in ? v : ((r >= nb && c == r) ? 1.0 : 0.0);
+        row[c] = in ? v : ((inv ? c == r - NB : (r >= nb && c == r)) ? e : 0.0);
       }
     }
     double s = 0.0;
@@ -391,8 +397,7 @@ struct CtaBand {
       }
       row[c] = lrc;
       double* dc = D + c * kLDD;  // column c of L11 (rows < c: don't-care)
-      if (r < NB) dc[r] = lrc;
-      if (r == 0) Dinv[c] = rs;
+      *(inv ? lbuf + (r - NB) : dc + r) = lrc;  // lanes >= NB: scratch, no branch
       __syncwarp();
       // rank-1 update of the rest of the row; entries right of the diagonal become
       // garbage that is never read (only c2 <= r is used or stored)
@@ -422,37 +427,14 @@ struct CtaBand {
       bw[slot_from(s0, j0, j0 + r)] = s;
       rhs[j0 + r] = s;
     }
-    invert_diag();
-    return -1;
-  }
-
-  // Warp 0, after the POTRF: D <- L11^-1 (row-major, D[i*kLDD + j] = Linv(i, j)), so the
-  // panel TRSM becomes a tensor-core product.  Lane j forward-substitutes L11 x = e_j
-  // with the pivots' reciprocals from Dinv; padded rows of a short block are identity
-  // rows and invert to themselves.  Runs inside the lookahead window, off the chain.
-  __device__ void invert_diag() {
-    const int j = threadIdx.x & 31;
-    double t[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) t[i] = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      t[k] *= Dinv[k];
-      const double* dk = D + k * kLDD;
-#pragma unroll
-      for (int h = 0; h < NB / 2; ++h) {
-        if (2 * h + 1 > k) {
-          const double2 l2 = reinterpret_cast<const double2*>(dk)[h];
-          if (2 * h > k) t[2 * h] = fma(-l2.x, t[k], t[2 * h]);
-          t[2 * h + 1] = fma(-l2.y, t[k], t[2 * h + 1]);
-        }
-      }
-    }
+    // D <- L11^-1, row-major (D[i*kLDD + j] = Linv(i, j)), once every lane is done
+    // reading L11 from it
     __syncwarp();
-    if (j < NB) {
+    if (inv) {
 #pragma unroll
-      for (int i = 0; i < NB; ++i) D[i * kLDD + j] = t[i];
+      for (int i = 0; i < NB; ++i) D[i * kLDD + (r - NB)] = row[i];
     }
+    return -1;
   }
 
   // Panel TRSM as a product: X = A L11^-T for the m panel rows, 16-row tiles over the
@@ -512,8 +494,9 @@ struct CtaBand {
   // and 4) is left to the POTRF warp.
   __device__ void update_tiles(int s0, int j0, int nb, int m, int tj_lo, int tj_hi, int w_lo) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp < w_lo || (w_lo == 1 && warp == 4)) return;
-    const int wid = (w_lo == 1) ? (warp < 4 ? warp - 1 : warp - 2) : warp;  // rank among the workers
+    if (w_lo == 1 && (warp & 3) == pw) return;
+    // rank among the workers
+    const int wid = (w_lo == 1) ? warp - (warp > pw) - (warp > pw + 4) : warp;
     const int nw = (w_lo == 1) ? kCtaWarps - 2 : kCtaWarps;
     const int gr = lane >> 2, gc = lane & 3;
     const int base = j0 + nb;
@@ -603,16 +586,16 @@ struct CtaBand {
       if (kd < NB && pending) wait_cols();  // the last prefetch overlaps this panel
       // warp_uniform(): tell ptxas the branch cannot split a warp, so the POTRF's
       // shuffles compile to plain SHFL instead of collective divergence handling
-      if (warp_uniform(warp) == 0) {
+      if (warp_uniform(warp) == pw) {
         trace_stamp(step, 3);
         const int f = potrf_diag(s0, j0, nb);
-        if (threadIdx.x == 0) s_fail = f;
+        if ((threadIdx.x & 31) == 0) s_fail = f;
         trace_stamp(step, 4);
       }
 #ifdef BCG_SERIAL_LOOKAHEAD
       __syncthreads();
 #endif
-      if (warp != 0 && jp >= 0) {
+      if (warp != pw && jp >= 0) {
         update_tiles(sp, jp, nbp, mp, NB / 16, 1 << 20, 1);
         if (warp == 1) trace_stamp(step, 5);
       }

@@ -35,6 +35,7 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, i
     w.bars = bars;
     w.bphase = bphase;
     w.phase = phase;
+    w.pw = ((blockIdx.x / 148) & 1) ? 2 : 0;
     w.tr = (blockIdx.x == 0 && mat == 0) ? g_trace : nullptr;
     w.ab = ab0 + (int64_t)mat * stride_ab;
     w.rhs = kSolve ? b0 + (int64_t)mat * stride_b : nullptr;
