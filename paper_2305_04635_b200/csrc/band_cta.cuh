@@ -502,53 +502,57 @@ struct CtaBand {
     const int base = j0 + nb;
     const int T = (m + 15) >> 4;
     tj_hi = min(tj_hi, T);
-    int idx = 0;
-    for (int tj = tj_lo; tj < tj_hi; ++tj) {
-      // this lane's 4 columns of the tile column, as window offsets minus the row
+    // this warp's tiles: every nw-th of the (tj, ti >= tj) sequence, starting at wid
+    int tj = tj_lo, ti = tj_lo + wid;
+    while (tj < tj_hi && ti >= T) { ti += tj + 1 - T; ++tj; }
+    while (tj < tj_hi) {
+      const int i0 = ti * 16, q0 = tj * 16;
+      // this lane's 4 columns of the tile, as window offsets minus the row
       int cb[2][2];
 #pragma unroll
       for (int v = 0; v < 2; ++v)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int q = tj * 16 + v * 8 + 2 * gc + e;
+          const int q = q0 + v * 8 + 2 * gc + e;
           cb[v][e] = slot_from(s0, j0, base + (q < m ? q : 0)) * g.lds - q;
         }
-      for (int ti = tj; ti < T; ++ti, ++idx) {
-        if (idx % nw != wid) continue;
-        const int i0 = ti * 16, q0 = tj * 16;
-        double acc[2][2][2];
-        bool ok[2][2][2];
+      double acc[2][2][2];
+      // interior tile (below the diagonal, every row < m): no masks
+      const bool full = ti > tj && i0 + 16 <= m;
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
+            const bool ok = full || ((i < m) && (q <= i));
+            acc[u][v][e] = ok ? win[cb[v][e] + i] : 0.0;
+          }
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        const double* pk = P + (k0 + gc) * g.pld;
+        double a[2], b[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) a[u] = -pk[i0 + u * 8 + gr];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) b[v] = pk[q0 + v * 8 + gr];
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int v = 0; v < 2; ++v)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
-              ok[u][v][e] = (i < m) && (q <= i);
-              acc[u][v][e] = ok[u][v][e] ? win[cb[v][e] + i] : 0.0;
-            }
-#pragma unroll
-        for (int k0 = 0; k0 < NB; k0 += 4) {
-          const double* pk = P + (k0 + gc) * g.pld;
-          double a[2], b[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) a[u] = -pk[i0 + u * 8 + gr];
-#pragma unroll
-          for (int v = 0; v < 2; ++v) b[v] = pk[q0 + v * 8 + gr];
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-#pragma unroll
-            for (int v = 0; v < 2; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], b[v]);
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int v = 0; v < 2; ++v)
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-              if (ok[u][v][e]) win[cb[v][e] + i0 + u * 8 + gr] = acc[u][v][e];
+          for (int v = 0; v < 2; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], b[v]);
       }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
+            if (full || ((i < m) && (q <= i))) win[cb[v][e] + i] = acc[u][v][e];
+          }
+      ti += nw;
+      while (tj < tj_hi && ti >= T) { ti += tj + 1 - T; ++tj; }
     }
   }
 
