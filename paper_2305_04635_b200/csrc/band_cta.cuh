@@ -172,7 +172,7 @@ struct CtaBand {
   double* Dinv;              // NB doubles of scratch (+ lbuf: the backward sweep's far sums)
   double* lbuf;              // 32 doubles: sink for the inverse lanes' column stores
   double* bw;                // ring of rhs / solution entries, slot(i) like columns
-  double* yb;                // backward sweep: nbuf x NB staged y entries
+  double* yb;                // backward sweep: nbuf x NB staged y entries; factor: y of the last two blocks
   unsigned long long* bars;  // mbarriers: [0] window loads, [1 + k] backward buffer k
   unsigned* bphase;          // smem: parity of the next wait on bars[1 + k]
   unsigned phase = 0;        // parity of the next wait on bars[0] (uniform register)
@@ -426,6 +426,7 @@ struct CtaBand {
     if (kSolve && r < nb) {
       bw[slot_from(s0, j0, j0 + r)] = s;
       rhs[j0 + r] = s;
+      yb[((j0 / NB) & 1) * NB + r] = s;  // y of this block for update_rhs (ring slot is reused)
     }
     // D <- L11^-1, row-major (D[i*kLDD + j] = Linv(i, j)), once every lane is done
     // reading L11 from it
@@ -488,24 +489,18 @@ struct CtaBand {
     }
   }
 
-  // Trailing update of 16x16 tiles (ti >= tj) with tile column tj in [tj_lo, tj_hi),
-  // by warps [w_lo, kCtaWarps).  C(i,j) -= sum_c P(i,c) P(j,c), i,j < m, lower only.
-  // w_lo == 1: the lookahead phase, run by warps 1-3 and 5-7 so that SMSP 0 (warps 0
-  // and 4) is left to the POTRF warp.
-  __device__ void update_tiles(int s0, int j0, int nb, int m, int tj_lo, int tj_hi, int w_lo) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (w_lo == 1 && (warp & 3) == pw) return;
-    // rank among the workers
-    const int wid = (w_lo == 1) ? warp - (warp > pw) - (warp > pw + 4) : warp;
-    const int nw = (w_lo == 1) ? kCtaWarps - 2 : kCtaWarps;
+  // Trailing update of 16x16 tiles, C(i,j) -= sum_c P(i,c) P(j,c), i,j < m, lower only.
+  // Tiles are numbered column by column ((0,0), (1,0), ..., (T-1,0), (1,1), ...); the
+  // calling warp (rank wid of nw workers) takes tiles first + wid, first + wid + nw, ...
+  // below `last`.
+  __device__ void update_tiles(int s0, int j0, int nb, int m, int first, int last, int wid, int nw) {
+    const int lane = threadIdx.x & 31;
     const int gr = lane >> 2, gc = lane & 3;
     const int base = j0 + nb;
     const int T = (m + 15) >> 4;
-    tj_hi = min(tj_hi, T);
-    // this warp's tiles: every nw-th of the (tj, ti >= tj) sequence, starting at wid
-    int tj = tj_lo, ti = tj_lo + wid;
-    while (tj < tj_hi && ti >= T) { ti += tj + 1 - T; ++tj; }
-    while (tj < tj_hi) {
+    int tj = 0, ti = first + wid, left = last - first - wid;
+    while (tj < T && ti >= T) { ti += tj + 1 - T; ++tj; }
+    while (tj < T && left > 0) {
       const int i0 = ti * 16, q0 = tj * 16;
       // this lane's 4 columns of the tile, as window offsets minus the row
       int cb[2][2];
@@ -552,18 +547,21 @@ struct CtaBand {
             if (full || ((i < m) && (q <= i))) win[cb[v][e] + i] = acc[u][v][e];
           }
       ti += nw;
-      while (tj < tj_hi && ti >= T) { ti += tj + 1 - T; ++tj; }
+      left -= nw;
+      while (tj < T && ti >= T) { ti += tj + 1 - T; ++tj; }
     }
   }
 
   // Forward-sweep update of the trailing rhs entries: b_i -= sum_c P(i,c) y_c.
-  __device__ void update_rhs(int s0, int j0, int nb, int m) {
+  // Rows [lo, min(hi, m)) by threads tid, tid + nt, ...
+  __device__ void update_rhs(int s0, int j0, int nb, int m, int lo, int hi, int tid, int nt) {
     const int base = j0 + nb;
-    for (int i = threadIdx.x; i < m; i += kCtaThreads) {
+    hi = min(hi, m);
+    for (int i = lo + tid; i < hi; i += nt) {
       double s = 0.0;
 #pragma unroll
       for (int c = 0; c < NB; ++c)
-        if (c < nb) s = fma(P[c * g.pld + i], bw[slot_from(s0, j0, j0 + c)], s);
+        if (c < nb) s = fma(P[c * g.pld + i], yb[((j0 / NB) & 1) * NB + c], s);
       bw[slot_from(s0, j0, base + i)] -= s;
     }
   }
@@ -578,10 +576,13 @@ struct CtaBand {
     for (int idx = threadIdx.x; idx < NB * g.pld; idx += kCtaThreads) P[idx] = 0.0;
     load_cols(0, min(n, kd + NB));
     wait_cols();
-    // Loop rotated so that one call site factors every diagonal block: iteration k
-    // runs [warp 0: POTRF(k) || warps 1-7: rest of update(k-1)], then TRSM(k), the
-    // write-back of panel k, the part of update(k) that feeds POTRF(k+1), and the
-    // prefetch of the columns step k+1 brings into the window.
+    // Loop rotated so that one call site factors every diagonal block.  Iteration k:
+    //   warp pw:           tile (0,0) of update(k-1) -> POTRF(k) (+ L11^-1)
+    //   6 other warps:     the rest of update(k-1)            (warp pw+4 idles: it shares
+    //                                                          the POTRF's sub-partition)
+    //   barrier, TRSM(k) as a DMMA product (all warps), barrier,
+    //   write-back of panel k, prefetch of the columns step k+1 brings into the window.
+    // The per-step chain is POTRF -> TRSM -> one tile update; everything else overlaps.
     int jp = -NB, sp = 0, nbp = 0, mp = 0;  // previous step
     int j0 = 0, s0 = 0;
     for (;;) {
@@ -590,18 +591,25 @@ struct CtaBand {
       if (kd < NB && pending) wait_cols();  // the last prefetch overlaps this panel
       // warp_uniform(): tell ptxas the branch cannot split a warp, so the POTRF's
       // shuffles compile to plain SHFL instead of collective divergence handling
-      if (warp_uniform(warp) == pw) {
+      const int wu = warp_uniform(warp);
+      if (wu == pw) {
+        // the previous step's update of this block (tile (0,0)) and of its rhs rows,
+        // then POTRF: no CTA barrier between the TRSM that fed them and this POTRF
+        if (jp >= 0) {
+          update_tiles(sp, jp, nbp, mp, 0, 1, 0, 1);
+          if (kSolve) update_rhs(sp, jp, nbp, mp, 0, NB, threadIdx.x & 31, 32);
+          __syncwarp();
+        }
         trace_stamp(step, 3);
         const int f = potrf_diag(s0, j0, nb);
         if ((threadIdx.x & 31) == 0) s_fail = f;
         trace_stamp(step, 4);
-      }
-#ifdef BCG_SERIAL_LOOKAHEAD
-      __syncthreads();
-#endif
-      if (warp != pw && jp >= 0) {
-        update_tiles(sp, jp, nbp, mp, NB / 16, 1 << 20, 1);
-        if (warp == 1) trace_stamp(step, 5);
+      } else if ((wu & 3) != pw && jp >= 0) {
+        // the rest of the previous step's update, on the other three SM sub-partitions
+        const int wid = wu - (wu > pw) - (wu > pw + 4);
+        update_tiles(sp, jp, nbp, mp, 1, 1 << 20, wid, kCtaWarps - 2);
+        if (kSolve) update_rhs(sp, jp, nbp, mp, NB, 1 << 20, threadIdx.x - 32 * wu + 32 * wid, 32 * (kCtaWarps - 2));
+        if (wu == (pw + 1) % 4) trace_stamp(step, 5);
       }
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(step, 6);
@@ -619,13 +627,11 @@ struct CtaBand {
       else __syncthreads();
       if (threadIdx.x < 32) trace_stamp(step, 1);
       store_cols(j0, nb);
-      // part 1: tile columns touching the next panel, then the rhs
-      update_tiles(s0, j0, nb, m, 0, NB / 16, 0);
-      if (kSolve) update_rhs(s0, j0, nb, m);
-      __syncthreads();
-      if (threadIdx.x < 32) trace_stamp(step, 2);
+      // prefetch the columns step k+1 brings into the window (into the slots just
+      // written back, once the write-back has read them)
       const int jlo = j0 + NB + kd;
       if (jlo < n) load_cols(jlo, min(n, jlo + NB));
+      if (threadIdx.x < 32) trace_stamp(step, 2);
       if (j0 + nb >= n) break;
       jp = j0; sp = s0; nbp = nb; mp = m;
       j0 += nb;
