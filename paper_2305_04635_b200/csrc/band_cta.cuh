@@ -447,6 +447,7 @@ struct CtaBand {
     const int sw = g.nslot - s0;
     const int T = (m + 15) >> 4;
     for (int t = warp; t < T; t += kCtaWarps) {
+      const bool tail = 16 * t + 8 >= m;  // rows 16t+8.. are all past m
       double acc[2][NB / 8][2];
 #pragma unroll
       for (int u = 0; u < 2; ++u)
@@ -469,7 +470,8 @@ struct CtaBand {
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int v = 0; v < NB / 8; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], bf[v]);
+          for (int v = 0; v < NB / 8; ++v)
+            if (u == 0 || !tail) dmma884(acc[u][v][0], acc[u][v][1], a[u], bf[v]);
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -514,6 +516,7 @@ struct CtaBand {
       double acc[2][2][2];
       // interior tile (below the diagonal, every row < m): no masks
       const bool full = ti > tj && i0 + 16 <= m;
+      const bool diag = ti == tj, tail = i0 + 8 >= m;
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -532,10 +535,13 @@ struct CtaBand {
         for (int u = 0; u < 2; ++u) a[u] = -pk[i0 + u * 8 + gr];
 #pragma unroll
         for (int v = 0; v < 2; ++v) b[v] = pk[q0 + v * 8 + gr];
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) dmma884(acc[u][v][0], acc[u][v][1], a[u], b[v]);
+        // skip the 8x8 blocks that are all padding rows (past m) or all above the diagonal
+        dmma884(acc[0][0][0], acc[0][0][1], a[0], b[0]);
+        if (!diag) dmma884(acc[0][1][0], acc[0][1][1], a[0], b[1]);
+        if (!tail) {
+          dmma884(acc[1][0][0], acc[1][0][1], a[1], b[0]);
+          dmma884(acc[1][1][0], acc[1][1][1], a[1], b[1]);
+        }
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u)
