@@ -27,12 +27,14 @@
 //   * Backward sweep (fused solve): L is streamed back through the same ring with a
 //     cp.async pipeline several blocks deep.
 #pragma once
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace bcg {
 
 constexpr int kCtaThreads = 256;
+static_assert(kCtaThreads - 64 == 192, "cta_panel_doubles sizes the far partials for 192 threads");
 constexpr int kCtaWarps = kCtaThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
 // the thread that issues and waits on the window's bulk copies: lane 0 of the last warp,
@@ -146,15 +148,33 @@ __device__ __forceinline__ double rsqrt_nr(double p) {
   return y;
 }
 
+// Branch-free 1/d for finite d > 0: MUFU.RCP64H seed + two Newton steps.
+__device__ __forceinline__ double rcp_nr(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+
 struct CtaGeom {
   int n, kd, ldab;  // matrix geometry
   int lds, nslot;   // shared window: nslot column slots of lds doubles
   int pld;          // leading dimension of the dense panel P (>= kd rounded up to 16, = 4 mod 16)
 };
 
+// The panel buffer P; the backward sweep reuses it for two L11^-1 blocks.
+__host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom& g, bool solve) {
+  // backward: two L11^-1 blocks + the far partial sums ((kCtaThreads - 64) doubles)
+  const size_t p = (size_t)nb_block * g.pld, inv = 2 * (size_t)nb_block * (nb_block + 4) + 192;
+  return (solve && inv > p) ? inv : p;
+}
+
 // Shared-memory footprint (bytes) of one CTA for block size NB.
 __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g, bool solve) {
-  size_t d = (size_t)g.nslot * g.lds + (size_t)nb_block * g.pld + (size_t)nb_block * (nb_block + 4) + nb_block + 32;
+  size_t d = (size_t)g.nslot * g.lds + cta_panel_doubles(nb_block, g, solve) + (size_t)nb_block * (nb_block + 4) +
+             nb_block + 32;
   if (solve) d += (size_t)g.nslot + (size_t)(g.nslot / nb_block) * nb_block;  // rhs ring + staged y
   return d * sizeof(double) + 64;
 }
@@ -663,9 +683,10 @@ struct CtaBand {
   // Block b = columns [b*NB, b*NB+nb): s_j = y_j - sum_{i >= b*NB+nb} L(i,j) x_i, then the
   // upper-triangular solve L11^T x_b = s.  The sum splits into a "far" part (x of blocks
   // >= b+2, known one block early) and a "near" part (x of block b+1).  Iteration b runs
-  //   warp 0:     near(b) (16x16 GEMV) + triangular solve(b) with L11 in registers
-  //   warps 1-7:  far(b-1) for the next block, concurrently
-  // so the per-block critical path is the 16-step shuffle chain only.  L blocks (and the y
+  //   warp 0:     near(b) (16x16 GEMV) + x_b = L11^-T s_b as a product with L11^-1
+  //   warp 1:     L11^-1 of block b-1 (forward substitution, off the critical path)
+  //   warps 2-7:  far(b-1) for the next block, concurrently
+  // so the per-block critical path is two short dot products.  L blocks (and the y
   // entries) stream in with bulk copies, kDepth blocks ahead, one mbarrier per ring buffer.
   __device__ void backward() {
     const int n = g.n;
@@ -706,35 +727,88 @@ struct CtaBand {
         if (threadIdx.x == 0) mbar_expect_tx(bars + 1 + k, 0);
       }
     };
-    // far part of block b from x entries of blocks >= b+2 (warps 1-7)
+    double* li_buf = P;                        // 2 x L11^-1 (the panel buffer is free now)
+    double* part = P + 2 * NB * kLDD;          // far partial sums, kFarChunks x NB
+    constexpr int kFarThreads = kCtaThreads - 64, kFarChunks = kFarThreads / NB;
+    // far part of block b from x entries of blocks >= b+2 (warps 2-7): thread (chunk q,
+    // column c) sums rows o = o_lo + q, o_lo + q + kFarChunks, ... of column c; the
+    // chunk partials are added in a fixed order (deterministic) after a named barrier.
     auto far = [&](int b) {
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
       const int k = b % nbuf;
       const double* blk = win + (size_t)k * NB * g.lds;
       const int rlo = c0 + nb + NB;  // first row of block b+2
-      const int sx = rlo % g.nslot;
-      for (int c = warp - 1; c < nb; c += kCtaWarps - 1) {
+      const int t = threadIdx.x - 64;
+      const int c = t % NB, q = t / NB;
+      double acc = 0.0;
+      if (c < nb) {
         const int j = c0 + c;
         const int len = col_len(j);
         const double* colj = blk + c * g.lds;
-        double acc = 0.0;
-        for (int o = (rlo - j) + lane; o < len; o += 32) {
-          int sl = sx + (j + o - rlo);
-          if (sl >= g.nslot) sl -= g.nslot;
+        int sl = (rlo + q) % g.nslot;
+        for (int o = rlo - j + q; o < len; o += kFarChunks) {
           acc = fma(colj[o], bw[sl], acc);
+          sl += kFarChunks;
+          if (sl >= g.nslot) sl -= g.nslot;
         }
-#pragma unroll
-        for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(kFull, acc, sh);
-        if (lane == 0) sfar[(b & 1) * NB + c] = yb[k * NB + c] - acc;
       }
+      part[q * NB + c] = acc;
+      asm volatile("bar.sync 1, %0;" ::"n"(kFarThreads) : "memory");
+      if (t < nb) {
+        double sum = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < kFarChunks; ++qq) sum += part[qq * NB + t];
+        sfar[(b & 1) * NB + t] = yb[k * NB + t] - sum;
+      }
+    };
+    // L11^-1 of block b into buffer b & 1 (warp 1, one block ahead of its use): lane j
+    // forward-substitutes L11 x = e_j; columns past a short last block are identity.
+    // li[j*kLDD + i] = Linv(i, j), so warp 0's lane r finds column r contiguous.
+    auto invert_t = [&](auto whole_tag, int b) {
+      constexpr bool kWhole = decltype(whole_tag)::value;
+      const int c0 = b * NB;
+      const int nb = kWhole ? NB : min(NB, n - c0);
+      const double* blk = win + (size_t)(b % nbuf) * NB * g.lds;
+      const int j = lane;
+      double dk[NB];  // reciprocal pivots first: independent of each other
+#pragma unroll
+      for (int kk = 0; kk < NB; ++kk) dk[kk] = (kWhole || kk < nb) ? rcp_nr(blk[kk * g.lds]) : 1.0;
+      double t[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) t[i] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+      for (int kk = 0; kk < NB; ++kk) {
+        const double* col = blk + kk * g.lds;
+        t[kk] *= dk[kk];
+#pragma unroll
+        for (int i = kk + 1; i < NB; ++i) {
+          if (kWhole) {
+            t[i] = fma(-col[i - kk], t[kk], t[i]);
+          } else {
+            const bool in = i < nb && i - kk <= g.kd;
+            const double lv = col[in ? i - kk : 0];
+            t[i] = fma(in ? -lv : 0.0, t[kk], t[i]);
+          }
+        }
+      }
+      if (j < NB) {
+        double* li = li_buf + (b & 1) * NB * kLDD + j * kLDD;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) li[i] = t[i];
+      }
+    };
+    auto invert = [&](int b) {
+      if (min(NB, n - b * NB) == NB && g.kd >= NB - 1) invert_t(std::true_type{}, b);
+      else invert_t(std::false_type{}, b);
     };
     for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d);
     const int tb = nblk + 1;  // trace rows after the factorization's
     // prologue: far part of the last block (nothing beyond it)
     mbar_wait(bars + 1 + (nblk - 1) % nbuf, parity(nblk - 1));
     __syncthreads();
-    if (warp != 0) far(nblk - 1);
+    if (warp >= 2) far(nblk - 1);
+    else if (warp == 1) invert(nblk - 1);
     for (int b = nblk - 1; b >= 0; --b) {
       const int k = b % nbuf;
       const int c0 = b * NB;
@@ -746,10 +820,6 @@ struct CtaBand {
       if (warp == 0) {
         const double* blk = win + (size_t)k * NB * g.lds;
         const int r = lane;
-        // L11 column r below the diagonal -> registers; near rows of block b+1 as well
-        double lrow[NB];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) lrow[c] = (r < nb && c > r && c < nb && c - r <= g.kd) ? blk[r * g.lds + (c - r)] : 0.0;
         double v = r < nb ? sfar[(b & 1) * NB + r] : 0.0;
         if (r < nb) {
           // near part: rows c0+nb .. c0+nb+NB-1 (block b+1), in band for this column
@@ -768,21 +838,38 @@ struct CtaBand {
           }
           v -= a0 + a1;
         }
-        const double dinv = r < nb ? 1.0 / blk[r * g.lds] : 0.0;
+        // x_b = L11^-T s_b: lane r dots column r of L11^-1 with s (no sequential chain)
+        double* ss = lbuf + NB;  // (lbuf[0, NB) is the second half of sfar)
+        if (r < NB) ss[r] = v;
+        __syncwarp();
+        const double* li = li_buf + (b & 1) * NB * kLDD + (r < NB ? r : 0) * kLDD;
+        double x0 = 0.0, x1 = 0.0;
 #pragma unroll
-        for (int c = NB - 1; c >= 0; --c) {
-          if (c < nb) {
-            const double xc = __shfl_sync(kFull, v * dinv, c);
-            if (r == c) v = xc;
-            else v = fma(-lrow[c], xc, v);  // lrow[c] = 0 for c <= r
-          }
+        for (int c = 0; c < NB; c += 4) {
+          const double2 l01 = *reinterpret_cast<const double2*>(li + c);
+          const double2 l23 = *reinterpret_cast<const double2*>(li + c + 2);
+          const double2 s01 = *reinterpret_cast<const double2*>(ss + c);
+          const double2 s23 = *reinterpret_cast<const double2*>(ss + c + 2);
+          x0 = fma(l01.x, s01.x, x0);
+          x1 = fma(l01.y, s01.y, x1);
+          x0 = fma(l23.x, s23.x, x0);
+          x1 = fma(l23.y, s23.y, x1);
         }
+        v = x0 + x1;
+        __syncwarp();
         if (r < nb) {
           bw[(c0 + r) % g.nslot] = v;
           rhs[c0 + r] = v;
         }
+        trace_stamp(tb + b, 2);
       } else if (b >= 1) {
-        far(b - 1);
+        if (warp >= 2) {
+          far(b - 1);
+          if (warp == 2) trace_stamp(tb + b, 5);
+        } else {
+          invert(b - 1);
+          trace_stamp(tb + b, 4);
+        }
       }
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(tb + b, 3);

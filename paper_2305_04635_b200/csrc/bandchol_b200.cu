@@ -41,7 +41,7 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, i
     w.rhs = kSolve ? b0 + (int64_t)mat * stride_b : nullptr;
     double* p = smem;
     w.win = p; p += (size_t)g.nslot * g.lds;
-    w.P = p; p += (size_t)NB * g.pld;
+    w.P = p; p += cta_panel_doubles(NB, g, kSolve);
     w.D = p; p += NB * (NB + 4);
     w.Dinv = p; p += NB;
     w.lbuf = p; p += 32;

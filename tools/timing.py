@@ -188,10 +188,11 @@ def trace_bwd(batch=1):
     bw = t[nblk + 1: 2 * nblk + 1]
     med = lambda x: float(np.median(x))  # noqa: E731
     out = {"batch": batch, "factor_step": med(np.diff(f[:-2, 0])),
-           "bwd_wait": med(bw[:, 1] - bw[:, 0]), "bwd_dots": med(bw[:, 2] - bw[:, 1]),
-           "bwd_trisolve": med(bw[:, 3] - bw[:, 2]), "bwd_issue": med(bw[:, 4] - bw[:, 3]),
+           "bwd_wait": med(bw[:, 1] - bw[:, 0]), "bwd_warp0": med(bw[1:-1, 2] - bw[1:-1, 1]),
+           "bwd_invert": med(bw[1:-1, 4] - bw[1:-1, 1]), "bwd_far": med(bw[1:-1, 5] - bw[1:-1, 1]),
+           "bwd_sync": med(bw[:, 3] - bw[:, 1]),
            "bwd_block": med(bw[:-1, 0] - bw[1:, 0]),
-           "bwd_total_cycles": float(bw[0, 4] - bw[-1, 0]), "factor_total_cycles": float(f[-3, 0] - f[0, 0])}
+           "bwd_total_cycles": float(bw[0, 3] - bw[-1, 0]), "factor_total_cycles": float(f[-3, 0] - f[0, 0])}
     print(json.dumps(out), flush=True)
 
 
