@@ -38,6 +38,9 @@
 namespace bcg {
 
 constexpr int kMultiThreads = 256;
+#ifndef BCG_MULTI_PREFETCH
+#define BCG_MULTI_PREFETCH false  // fetch a worker's next ticket while its current task runs
+#endif
 
 struct MultiGeom {
   int n, kd, ldab;
@@ -49,7 +52,7 @@ struct MultiGeom {
 // ---- workspace ---------------------------------------------------------------------
 // [ctrl: 8 ints][tcnt: nblk*(T+1)][lrdy: nblk*(T+1)]
 struct MultiWs {
-  int* ctrl;  // [0] ticket, [1] fail (global column + 1)
+  int* ctrl;  // [0] ticket, [1] fail (global column + 1), [2] pivot's SM id + 1
   int* tcnt;
   int* lrdy;
 };
@@ -134,10 +137,11 @@ __device__ __forceinline__ void load_tile(double* s, const double* ab, const Mul
   }
 }
 
-template <int NB>
-__device__ __forceinline__ void store_tile(const double* s, double* ab, const MultiGeom& g, int R, int C) {
+template <int NB, int NT = kMultiThreads>
+__device__ __forceinline__ void store_tile(const double* s, double* ab, const MultiGeom& g, int R, int C,
+                                           int t = threadIdx.x) {
   constexpr int LD = MultiTile<NB>::LD;
-  for (int idx = threadIdx.x; idx < NB * NB; idx += kMultiThreads) {
+  for (int idx = t; idx < NB * NB; idx += NT) {
     const int c = idx / NB, r = idx - c * NB;
     const int i = R * NB + r, j = C * NB + c;
     if ((i < g.n) && (i >= j) && (i - j <= g.kd)) __stcg(ab + (int64_t)j * g.ldab + (i - j), s[c * LD + r]);
@@ -145,17 +149,19 @@ __device__ __forceinline__ void store_tile(const double* s, double* ab, const Mu
 }
 
 // ---- tile GEMM on the FP64 tensor path -------------------------------------------------
-// kSub: C -= A B^T (C read from sC)      else: C = A B^T.  All 8 warps, M = N = K = NB.
+// kSub: C -= A B^T (C read from sC)      else: C = A B^T.  NW warps (warp index wg within
+// the group, synchronised by named barrier bar_id over bar_cnt threads), M = N = K = NB.
 // A(m,k) = sA[k*LD + m], B(n,k) = sB[k*LD + n], C(m,n) = sC[n*LD + m].  sC must not alias sA/sB.
-template <int NB, bool kSub>
-__device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const double* sB) {
+template <int NB, bool kSub, int NW = 8>
+__device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const double* sB, int wg = threadIdx.x >> 5,
+                                          int bar_id = 0, int bar_cnt = kMultiThreads) {
   constexpr int LD = MultiTile<NB>::LD;
   constexpr int MT = NB / 8;
   constexpr int WM = (NB == 64) ? 2 : 4;  // warps along m
-  constexpr int WN = 8 / WM;
+  constexpr int WN = NW / WM;
   constexpr int TM = MT / WM, TN = MT / WN;
-  static_assert(TM >= 1 && TN >= 1, "tile too small for 8 warps");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  static_assert(TM >= 1 && TN >= 1, "tile too small for the warps");
+  const int warp = wg, lane = threadIdx.x & 31;
   const int wm = warp % WM, wn = warp / WM;
   const int gr = lane >> 2, gc = lane & 3;
   double acc[TM][TN][2];
@@ -182,7 +188,7 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
 #pragma unroll
       for (int tn = 0; tn < TN; ++tn) dmma884(acc[tm][tn][0], acc[tm][tn][1], a[tm], b[tn]);
   }
-  __syncthreads();  // sC may be read by other warps' fragment loads above (kSub) -- finish before writing
+  named_sync(bar_id, bar_cnt);  // sC may be read by other warps' fragment loads above (kSub)
 #pragma unroll
   for (int tm = 0; tm < TM; ++tm)
 #pragma unroll
@@ -191,7 +197,7 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
       sC[nn * LD + m] = acc[tm][tn][0];
       sC[(nn + 1) * LD + m] = acc[tm][tn][1];
     }
-  __syncthreads();
+  named_sync(bar_id, bar_cnt);
 }
 
 // ---- warp-level Cholesky of a 32x32 block in a smem tile (the pivot chain) ------------
@@ -263,14 +269,13 @@ __device__ __forceinline__ void trsm_rows(double* sX, const double* __restrict__
 }
 
 // ---- the kernel ------------------------------------------------------------------------
-template <int NB, int kPerSM>
+template <int NB, int kPerSM, int kGroups>
 __global__ void __launch_bounds__(kMultiThreads, kPerSM)
 band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* info) {
   static_assert(NB == 32, "the pivot chain is a 32-lane warp POTRF");
   extern __shared__ __align__(16) double smem[];
   constexpr int E = MultiTile<NB>::ELEMS;
   constexpr int LD = MultiTile<NB>::LD;
-  __shared__ int s_task;
   __shared__ int s_ok;
   __shared__ int s_fail;
   __shared__ double lbuf[32];
@@ -283,7 +288,10 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
     if (threadIdx.x < NB) sdinv[threadIdx.x] = 1.0 / sL[threadIdx.x * LD + threadIdx.x];
   };
 
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) st_release(ws.ctrl + 2, (int)smid + 1);
     // ------------------------------ pivot ---------------------------------------
     double* sD = smem;           // current diagonal tile (fully updated)
     double* sLp = smem + E;      // L(j, j-1) from the previous step
@@ -371,59 +379,140 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   }
 
   // -------------------------------- workers -------------------------------------------
-  double* sA = smem;
-  double* sB = smem + E;
-  double* sC = smem + 2 * E;
+  // The pivot's SM is left to the pivot: its chain is the critical path, and worker
+  // tiles on the same SM would compete for its issue slots and pipes.  (Cooperative
+  // launch: block 0 is resident, so its id appears.)
+  {
+    __shared__ int s_piv;
+    if (threadIdx.x == 0) {
+      int v;
+      while ((v = ld_acquire(ws.ctrl + 2)) == 0) __nanosleep(64);
+      s_piv = v - 1;
+    }
+    __syncthreads();
+    if (s_piv == (int)smid) return;
+  }
+  // kGroups independent warp groups per CTA (2 for wide bands), each with its own three
+  // tiles, its own named barrier and its own tickets: while one group waits on a flag or
+  // an L2 round trip the other computes.  The next ticket is fetched while the current
+  // task runs (a held, not-yet-started ticket cannot deadlock: the smallest unfinished
+  // ticket is always a group's current task, and its dependencies are all smaller).
+  constexpr int GT = kMultiThreads / kGroups, GW = GT / 32;
+  constexpr bool kPrefetchTicket = BCG_MULTI_PREFETCH;
+  const int grp = warp / GW, gt = threadIdx.x - grp * GT, wg = warp - grp * GW;
+  const int bar = 1 + grp;
+  __shared__ int s_task2[2], s_ok2[2];
+  __shared__ double sdinv2[2][NB];
+  double* sA = smem + grp * 3 * E;
+  double* sB = sA + E;
+  double* sC = sA + 2 * E;
   const int Q = g.Q;
   const long long total = (long long)nblk * Q;
+  int next_ticket = 0;
+  if (kPrefetchTicket && gt == 0) next_ticket = atomicAdd(ws.ctrl, 1);
+  auto gsync = [&]() { named_sync(bar, GT); };
+  auto gpublish = [&](int* flag, int value) {
+    gsync();
+    if (gt == 0) {
+      __threadfence();
+      st_release(flag, value);
+    }
+  };
+  // one thread: wait for up to three flags (issued together, then spun on one by one)
+  auto wait3 = [&](const int* f0, int v0, const int* f1, int v1, const int* f2, int v2) -> bool {
+    const int a0 = ld_acquire(f0), a1 = f1 ? ld_acquire(f1) : v1, a2 = f2 ? ld_acquire(f2) : v2;
+    if (a0 < v0 && !spin_ge(f0, v0, ws.ctrl + 1, 256)) return false;
+    if (a1 < v1 && !spin_ge(f1, v1, ws.ctrl + 1, 256)) return false;
+    if (a2 < v2 && !spin_ge(f2, v2, ws.ctrl + 1, 256)) return false;
+    return true;
+  };
+#ifdef BCG_TRACE
+  unsigned long long acc_ph[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+  auto ph = [&](int k) {
+    const long long now = clock64();
+    acc_ph[k] += (unsigned long long)(now - tprev);
+    tprev = now;
+  };
+#else
+  auto ph = [&](int) {};
+#endif
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(ws.ctrl, 1);
-    __syncthreads();
-    const long long t = warp_uniform(s_task);
+    if (gt == 0) {
+      if (kPrefetchTicket) {
+        s_task2[grp] = next_ticket;
+        next_ticket = atomicAdd(ws.ctrl, 1);
+      } else {
+        s_task2[grp] = atomicAdd(ws.ctrl, 1);
+      }
+    }
+    gsync();
+    const long long t = warp_uniform(s_task2[grp]);
     if (t >= total) break;
+    ph(0);
     const int j = (int)(t / Q), q = (int)(t - (long long)j * Q);
     if (q < T - 1) {
       // TRSM: L(R, j) = A(R, j) L(j,j)^-T
       const int R = j + 2 + q;
-      if (R >= nblk) { __syncthreads(); continue; }
-      if (threadIdx.x == 0)
-        s_ok = spin_ge(LR(j, 0), 1, ws.ctrl + 1, 256) &&
-               spin_ge(TC(R, R - j), j - max(0, R - T), ws.ctrl + 1, 256);
-      __syncthreads();
-      if (!warp_uniform(s_ok)) break;
-      load_tile<NB, kMultiThreads>(sA, ab, g, R, j, threadIdx.x);
-      load_tile<NB, kMultiThreads>(sB, ab, g, j, j, threadIdx.x);
-      __syncthreads();
-      make_dinv(sB);
-      __syncthreads();
-      if (warp == 0) trsm_rows<NB>(sA, sB, sdinv, threadIdx.x);
-      __syncthreads();
-      store_tile<NB>(sA, ab, g, R, j);
-      cta_publish(LR(R, R - j), 1);
+      if (R >= nblk) { gsync(); continue; }
+      if (gt == 0) s_ok2[grp] = wait3(LR(j, 0), 1, TC(R, R - j), j - max(0, R - T), nullptr, 0);
+      gsync();
+      if (!warp_uniform(s_ok2[grp])) break;
+      ph(1);
+      load_tile<NB, GT>(sA, ab, g, R, j, gt);
+      load_tile<NB, GT>(sB, ab, g, j, j, gt);
+      gsync();
+      ph(2);
+      if (gt < NB) sdinv2[grp][gt] = 1.0 / sB[gt * LD + gt];
+      gsync();
+      if (wg == 0) trsm_rows<NB>(sA, sB, sdinv2[grp], gt);
+      gsync();
+      store_tile<NB, GT>(sA, ab, g, R, j, gt);
+      ph(3);
+      gpublish(LR(R, R - j), 1);
+      ph(4);
     } else {
+      // update order within a step: first the tile column that feeds the next panel
+      // (S = j+1, R = j+1..j+T) -- the next step's TRSMs wait on exactly these -- then
+      // the rest row by row from the diagonal (a = R-j-1 >= 1, b = R-S < a)
       const int u = q - (T - 1);
-      int a = (int)((sqrtf(8.0f * (float)u + 1.0f) - 1.0f) * 0.5f);
-      while (a * (a + 1) / 2 > u) --a;
-      while ((a + 1) * (a + 2) / 2 <= u) ++a;
-      const int b = u - a * (a + 1) / 2;
+      int a, b;
+      if (u < T) {
+        a = u;
+        b = u;
+      } else {
+        const int v = u - T;
+        a = (int)((sqrtf(8.0f * (float)v + 1.0f) + 1.0f) * 0.5f);
+        while (a * (a - 1) / 2 > v) --a;
+        while ((a + 1) * a / 2 <= v) ++a;
+        b = v - a * (a - 1) / 2;
+      }
       const int R = j + 1 + a, S = R - b;
       const bool pivot_owned = (R == j + 1) || (R == j + 2 && S >= j + 1);
-      if (R >= nblk || pivot_owned) { __syncthreads(); continue; }
+      if (R >= nblk || pivot_owned) { gsync(); continue; }
       const int done = j - max(0, R - T);
-      if (threadIdx.x == 0)
-        s_ok = spin_ge(LR(R, R - j), 1, ws.ctrl + 1, 256) && spin_ge(LR(S, S - j), 1, ws.ctrl + 1, 256) &&
-               spin_ge(TC(R, R - S), done, ws.ctrl + 1, 256);
-      __syncthreads();
-      if (!warp_uniform(s_ok)) break;
-      load_tile<NB, kMultiThreads>(sA, ab, g, R, j, threadIdx.x);
-      load_tile<NB, kMultiThreads>(sB, ab, g, S, j, threadIdx.x);
-      load_tile<NB, kMultiThreads>(sC, ab, g, R, S, threadIdx.x);
-      __syncthreads();
-      tile_gemm<NB, true>(sC, sA, sB);
-      store_tile<NB>(sC, ab, g, R, S);
-      cta_publish(TC(R, R - S), done + 1);
+      if (gt == 0)
+        s_ok2[grp] = wait3(LR(R, R - j), 1, LR(S, S - j), 1, TC(R, R - S), done);
+      gsync();
+      if (!warp_uniform(s_ok2[grp])) break;
+      ph(1);
+      load_tile<NB, GT>(sA, ab, g, R, j, gt);
+      load_tile<NB, GT>(sB, ab, g, S, j, gt);
+      load_tile<NB, GT>(sC, ab, g, R, S, gt);
+      gsync();
+      ph(2);
+      tile_gemm<NB, true, GW>(sC, sA, sB, wg, bar, GT);
+      store_tile<NB, GT>(sC, ab, g, R, S, gt);
+      ph(3);
+      gpublish(TC(R, R - S), done + 1);
+      ph(4);
     }
   }
+#ifdef BCG_TRACE
+  // worker phase totals (cycles, summed over groups): ticket, deps, loads, compute, publish
+  if (gt == 0 && g_trace && g_trace_cap > 8)
+    for (int k = 0; k < 5; ++k) atomicAdd(g_trace + g_trace_cap - 8 + k, acc_ph[k]);
+#endif
 }
 
 // ---- host side -------------------------------------------------------------------------
@@ -449,13 +538,14 @@ inline size_t multi_workspace_bytes(int n, int kd) {
 
 // Occupancy: wide bands (many worker tasks per step) run 3 CTAs per SM for latency
 // hiding; narrower bands keep 2 so the pivot CTA gets the registers of its chain.
-template <int kPerSM>
+template <int kPerSM, int kGroups>
 inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, void* workspace, int sms,
                           cudaStream_t st, char* err, size_t errlen) {
   constexpr int NB = kMultiNB;
   MultiGeom g = multi_geom(n, kd, ldab);
-  const size_t smem = 5 * (size_t)MultiTile<NB>::ELEMS * sizeof(double);
-  auto k = band_multi_kernel<NB, kPerSM>;
+  // pivot: 5 tiles; workers: 3 per group
+  const size_t smem = (size_t)(kGroups == 1 ? 5 : 3 * kGroups) * MultiTile<NB>::ELEMS * sizeof(double);
+  auto k = band_multi_kernel<NB, kPerSM, kGroups>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) {
     snprintf(err, errlen, "cudaFuncSetAttribute(band_multi): %s", cudaGetErrorString(e));
@@ -486,8 +576,8 @@ inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, vo
 
 inline int launch_multi(double* ab, int n, int kd, int ldab, int32_t* info, void* workspace, int sms,
                         cudaStream_t st, char* err, size_t errlen) {
-  if (kd >= 1000) return launch_multi_t<3>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
-  return launch_multi_t<2>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
+  if (kd >= 1000) return launch_multi_t<3, 2>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
+  return launch_multi_t<2, 1>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
 }
 
 }  // namespace bcg

@@ -124,6 +124,10 @@ def trace(tag):
         v = d[:-1, i]
         out[nm] = float(np.median(v))
     out["gap"] = float(np.median(nxt))
+    wk = t[-8:-3].astype(np.float64)
+    if wk.sum() > 0:
+        out["worker_share"] = {k: round(float(v / wk.sum()), 3)
+                               for k, v in zip(["ticket", "deps", "loads", "compute_store", "publish"], wk)}
     print(json.dumps(out), flush=True)
 
 
