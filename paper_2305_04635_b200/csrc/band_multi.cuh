@@ -201,23 +201,35 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
 }
 
 // ---- warp-level Cholesky of a 32x32 block in a smem tile (the pivot chain) ------------
-// s(r, c) = s[c*ld + r], lower part valid.  Same redundant-chain scheme as
-// CtaBand::potrf_diag: every lane computes the pivot sequence, lane r owns row r.
-// Writes L back (lower), returns the failing local column or -1 (uniform).
+// s(r, c) = s[c*ld + r], lower part valid; ld*8 bytes must keep columns 16-byte aligned.
+// Same scheme as CtaBand::potrf_diag: every lane computes the pivot sequence (branch-free
+// Newton rsqrt, the next column's operands broadcast a column early), lane r owns row r.
+// Column c of L is written straight into its tile column, which then serves as the
+// broadcast buffer of the rank-1 update (one __syncwarp per column); entries above the
+// diagonal become don't-care.  Rows past nvalid are identity rows.  Failure: after a bad
+// pivot every later pivot is NaN, so the failing column is the first lane whose L(r, r)
+// is not > 0.  Returns it or -1 (uniform).
 __device__ __forceinline__ int warp_potrf32(double* s, int ld, int nvalid, double* lbuf) {
+  (void)lbuf;
   const int r = threadIdx.x & 31;
   double row[32];
+  if (nvalid == 32) {
 #pragma unroll
-  for (int c = 0; c < 32; ++c) row[c] = (c <= r && r < nvalid) ? s[c * ld + r] : ((c == r) ? 1.0 : 0.0);
+    for (int c = 0; c < 32; ++c) row[c] = s[c * ld + r];
+  } else {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const double v = s[c * ld + r];
+      row[c] = (r < nvalid) ? v : ((c == r) ? 1.0 : 0.0);
+    }
+  }
   double p = __shfl_sync(kFull, row[0], 0);
   double alpha = __shfl_sync(kFull, row[0], 1);
   double beta = __shfl_sync(kFull, row[1], 1);
   double rs = rsqrt_nr(p);
-  int fail = -1;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
-    if (fail < 0 && c < nvalid && !(p > 0.0)) fail = c;
-    const double lrc = (r > c) ? row[c] * rs : 0.0;
+    const double lrc = row[c] * rs;  // L(r, c) for r >= c (lane c: p * rs bit for bit)
     const double l1 = alpha * rs;
     const double pn = fma(-l1, l1, beta);
     const double rsn = rsqrt_nr(pn);
@@ -225,28 +237,30 @@ __device__ __forceinline__ int warp_potrf32(double* s, int ld, int nvalid, doubl
     double alpha_n = 0.0, beta_n = 0.0;
     if (c + 2 < 32) {
       const double bn = fma(-lrc, lrc, row[c + 2 < 32 ? c + 2 : 0]);
-      alpha_n = __shfl_sync(kFull, row[c + 1 < 32 ? c + 1 : 0], c + 2);
-      beta_n = __shfl_sync(kFull, bn, c + 2);
+      alpha_n = shfl_early(row[c + 1 < 32 ? c + 1 : 0], c + 2);
+      beta_n = shfl_early(bn, c + 2);
     }
-    if (r == c) row[c] = p * rs;
-    else if (r > c) row[c] = lrc;
-    lbuf[r] = lrc;
+    row[c] = lrc;
+    double* sc = s + c * ld;
+    sc[r] = lrc;
     __syncwarp();
 #pragma unroll
-    for (int c2 = c + 2; c2 < 32; ++c2) row[c2] = fma(-lrc, lbuf[c2], row[c2]);
-    __syncwarp();
+    for (int h = 0; h < 16; ++h) {
+      if (2 * h + 1 >= c + 2) {
+        const double2 l2 = reinterpret_cast<const double2*>(sc)[h];
+        if (2 * h >= c + 2) row[2 * h] = fma(-lrc, l2.x, row[2 * h]);
+        row[2 * h + 1] = fma(-lrc, l2.y, row[2 * h + 1]);
+      }
+    }
     p = pn;
     rs = rsn;
     alpha = alpha_n;
     beta = beta_n;
   }
-  if (fail < 0 && r < nvalid) {
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-      if (c <= r) s[c * ld + r] = row[c];
-  }
+  const double dgl = (r < nvalid) ? s[r * ld + r] : 1.0;
+  const unsigned bad = __ballot_sync(kFull, !(dgl > 0.0));
   __syncwarp();
-  return fail;
+  return bad ? __ffs(bad) - 1 : -1;
 }
 
 // ---- TRSM of a tile by substitution: X <- X L^-T (L lower NB x NB), row per thread ------
