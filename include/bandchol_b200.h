@@ -83,6 +83,16 @@ int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t s
  * next panel published).  NULL disables tracing. */
 int bcg_set_trace(void* device_buffer, size_t bytes);
 
+/* Backward error ||A - L L^T||_F / ||A||_F over the band, on the device: the GPU
+ * restatement of the reference's residual_norm (pkg/src/bandchol/core.py:186-213) --
+ * off-diagonal entries weighted twice, result 0 for A = 0 = L L^T, +inf for A = 0 != L L^T.
+ * a: the original matrix (lda), l: its factor (ldl), both device AB storage; *result
+ * (device) receives the residual.  Deterministic (fixed-order reductions in workspace,
+ * >= bcg_band_residual_workspace_size() bytes).  Asynchronous on stream. */
+size_t bcg_band_residual_workspace_size(void);
+int bcg_band_residual(int64_t n, int64_t kd, const double* a, int64_t lda, const double* l, int64_t ldl,
+                      double* result, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Measurement utility (bench.py): FP64 FMA-pipe peak of the current device in
  * TFLOP/s, from a register-only DFMA loop over every SM (synchronous, ~10 ms).
  * The roofline denominator for the FP64-bound configs. */

@@ -13,6 +13,8 @@ from .engine import (BatchedBandSolver, TraceEvent, pinned_empty, dpbsv_batched_
                      dpbtrs_batched_device, dpbtrs_device, factor_batched,
                      factor_blocked_parallel, factor_blocked_serial, factor_solve_batched,
                      library_version, solve_batched, solve_with_factor)
+from .engine import band_residual_device, residual_norm
+from .fixtures import load_matrix, load_matrix_device, save_matrix
 from .errors import (BandCholError, BandwidthNotDivisible, CountOverflow, DeviceError,
                      GridTooSmall, InvalidBandwidth, NotPositiveDefinite, OutOfBand,
                      ShapeMismatch, SingularFactor)
@@ -29,4 +31,5 @@ __all__ = [
     "DeviceError", "GridTooSmall", "InvalidBandwidth", "NotPositiveDefinite", "OutOfBand",
     "ShapeMismatch", "SingularFactor", "flops_approx", "flops_exact", "flops_model", "CONFIGS",
     "BandConfig", "generate_spd", "generate_spd_wide", "make_rhs",
+    "band_residual_device", "residual_norm", "load_matrix", "load_matrix_device", "save_matrix",
 ]

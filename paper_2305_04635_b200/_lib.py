@@ -28,6 +28,8 @@ SIGNATURES = {
     "bcg_dpbsv_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _vp]),
     "bcg_probe_fp64_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
     "bcg_set_trace": (ctypes.c_int, [_vp, _sz]),
+    "bcg_band_residual_workspace_size": (_sz, []),
+    "bcg_band_residual": (ctypes.c_int, [_i64, _i64, _dp, _i64, _dp, _i64, _dp, _vp, _sz, _vp]),
 }
 
 _lib = None

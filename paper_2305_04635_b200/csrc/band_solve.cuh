@@ -42,8 +42,21 @@ __device__ void band_forward(const double* __restrict__ ab, int n, int kd, int l
     double s = 0.0;
     const int lbeg = max(0, r0 - kd);
     if (lane < nb) {
-      for (int l = lbeg + warp; l < r0; l += kCtaThreads / 32)
-        if (i - l <= kd) s = fma(ab[(int64_t)l * ldab + (i - l)], b[l], s);
+      // four independent chains so the L2/HBM loads of a row overlap
+      constexpr int W = kCtaThreads / 32;
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int l = max(lbeg, i - kd) + warp;  // columns in band for row i
+      for (; l + 3 * W < r0; l += 4 * W) {
+        const double a0 = ab[(int64_t)l * ldab + (i - l)], a1 = ab[(int64_t)(l + W) * ldab + (i - l - W)];
+        const double a2 = ab[(int64_t)(l + 2 * W) * ldab + (i - l - 2 * W)];
+        const double a3 = ab[(int64_t)(l + 3 * W) * ldab + (i - l - 3 * W)];
+        s = fma(a0, b[l], s);
+        s1 = fma(a1, b[l + W], s1);
+        s2 = fma(a2, b[l + 2 * W], s2);
+        s3 = fma(a3, b[l + 3 * W], s3);
+      }
+      for (; l < r0; l += W) s = fma(ab[(int64_t)l * ldab + (i - l)], b[l], s);
+      s += (s1 + s2) + s3;
     }
     red[warp][lane] = s;
     __syncthreads();
@@ -56,7 +69,7 @@ __device__ void band_forward(const double* __restrict__ ab, int n, int kd, int l
       for (int c = 0; c < NB; ++c)
         row[c] = (lane < nb && c <= lane && lane - c <= kd) ? ab[(int64_t)(r0 + c) * ldab + (lane - c)] : 0.0;
       double v = lane < nb ? b[i] - t : 0.0;
-      const double dinv = lane < nb ? 1.0 / ab[(int64_t)i * ldab] : 0.0;
+      const double dinv = lane < nb ? rcp_nr(ab[(int64_t)i * ldab]) : 0.0;
 #pragma unroll
       for (int c = 0; c < NB; ++c) {
         if (c < nb) {
@@ -84,8 +97,15 @@ __device__ void band_backward(const double* __restrict__ ab, int n, int kd, int 
       const int j = c0 + c;
       const double* colj = ab + (int64_t)j * ldab;
       const int len = min(kd, n - 1 - j) + 1;
-      double s = 0.0;
-      for (int o = nb - c + lane; o < len; o += 32) s = fma(colj[o], b[j + o], s);
+      double s = 0.0, s1 = 0.0;
+      int o = nb - c + lane;
+      for (; o + 32 < len; o += 64) {
+        const double a0 = colj[o], a1 = colj[o + 32];
+        s = fma(a0, b[j + o], s);
+        s1 = fma(a1, b[j + o + 32], s1);
+      }
+      if (o < len) s = fma(colj[o], b[j + o], s);
+      s += s1;
 #pragma unroll
       for (int sh = 16; sh > 0; sh >>= 1) s += __shfl_xor_sync(kFull, s, sh);
       if (lane == 0) sv[c] = b[j] - s;
@@ -94,7 +114,7 @@ __device__ void band_backward(const double* __restrict__ ab, int n, int kd, int 
     __syncthreads();
     if (warp == 0) {
       double v = lane < nb ? sv[lane] : 0.0;
-      const double dinv = lane < nb ? 1.0 / dblk[lane][lane] : 0.0;
+      const double dinv = lane < nb ? rcp_nr(dblk[lane][lane]) : 0.0;
 #pragma unroll
       for (int c = NB - 1; c >= 0; --c) {
         if (c < nb) {

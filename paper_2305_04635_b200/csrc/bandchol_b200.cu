@@ -13,6 +13,7 @@
 #include "../../include/bandchol_b200.h"
 #include "band_cta.cuh"
 #include "band_solve.cuh"
+#include "band_residual.cuh"
 #include "band_multi.cuh"
 
 namespace bcg {
@@ -361,4 +362,28 @@ extern "C" int bcg_probe_fp64_peak(double* tflops) {
   if (e != cudaSuccess) return cuda_status(e, "dfma_probe_kernel");
   *tflops = 2.0 * 64.0 * iters * (double)blocks * tpb / (best * 1e-3) / 1e12;
   return 0;
+}
+
+// ---- device residual --------------------------------------------
+static int residual_blocks() { return sm_count() * 8; }
+
+extern "C" size_t bcg_band_residual_workspace_size(void) {
+  return (size_t)residual_blocks() * 2 * sizeof(double);
+}
+
+extern "C" int bcg_band_residual(int64_t n, int64_t kd, const double* a, int64_t lda, const double* l, int64_t ldl,
+                                 double* result, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int r = check_geom(n, kd, lda)) return r;
+  if (ldl < kd + 1 || ldl > INT_MAX / 2) return fail_arg(6, "ldl=%lld < kd+1", (long long)ldl);
+  if (!a) return fail_arg(3, "a is NULL");
+  if (!l) return fail_arg(5, "l is NULL");
+  if (!result) return fail_arg(7, "result is NULL");
+  const int blocks = residual_blocks();
+  if (!workspace || workspace_bytes < (size_t)blocks * 2 * sizeof(double))
+    return fail_arg(8, "workspace smaller than bcg_band_residual_workspace_size()");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = (double*)workspace;
+  bcg::band_residual_kernel<<<blocks, bcg::kResidThreads, 0, st>>>((int)n, (int)kd, a, (int)lda, l, (int)ldl, part);
+  bcg::band_residual_finish<<<1, 32, 0, st>>>(part, blocks, result);
+  return cuda_status(cudaGetLastError(), "band_residual_kernel launch");
 }

@@ -152,6 +152,36 @@ def dpbsv_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=Non
     return info
 
 
+def band_residual_device(a, l, n: int, kd: int, lda: int, ldl: int, out=None, stream=None):
+    """Device ||A - L L^T||_F / ||A||_F (core.py:186-213) of CUDA float64 tensors; returns
+    a 1-element CUDA tensor (no host synchronisation)."""
+    torch = _torch()
+    lib = _lib.load()
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=a.device)
+    need = int(lib.bcg_band_residual_workspace_size())
+    ws = torch.empty(need // 8 + 1, dtype=torch.float64, device=a.device)
+    rc = lib.bcg_band_residual(n, kd, a.data_ptr(), lda, l.data_ptr(), ldl, out.data_ptr(), ws.data_ptr(),
+                               need, _stream_handle(torch, stream))
+    _lib.check(rc, "bcg_band_residual")
+    return out
+
+
+def residual_norm(original, factor) -> float:
+    """residual_norm(original, factor) of the reference (core.py:186-213), computed on the GPU."""
+    check_matrix(original)
+    check_matrix(factor)
+    if original.dim != factor.dim or original.bandwidth != factor.bandwidth:
+        raise ShapeMismatch(
+            f"matrix ({original.dim}, k={original.bandwidth}) vs "
+            f"factor ({factor.dim}, k={factor.bandwidth})")
+    torch = _torch()
+    a = torch.from_numpy(np.ascontiguousarray(original.data)).to("cuda")
+    f = torch.from_numpy(np.ascontiguousarray(factor.data)).to("cuda")
+    r = band_residual_device(a, f, original.dim, original.bandwidth, original.lead_dim, factor.lead_dim)
+    return float(r.item())
+
+
 def _raise_factor_info(info_value: int) -> None:
     if info_value > 0:
         raise NotPositiveDefinite(info_value - 1)
@@ -282,6 +312,7 @@ def library_version() -> int:
 
 
 __all__ = [
+    "band_residual_device", "residual_norm",
     "TraceEvent", "dpbtrf_device", "dpbtrf_batched_device", "dpbtrs_device", "dpbtrs_batched_device",
     "dpbsv_batched_device", "factor_blocked_serial", "factor_blocked_parallel", "solve_with_factor",
     "factor_batched", "factor_solve_batched", "solve_batched", "library_version",
