@@ -323,7 +323,7 @@ def run_gpu_arm(args) -> int:
     value = flops_total * args.steps / (max_ms * 1e-3) / 1e9  # GFLOP/s, whole job
 
     # end to end through the public API with host buffers (pinned), per rank shard
-    solver = bc.BatchedBandSolver(nb, n, kd, chunks=8) if cfg.batch > 1 else None
+    solver = bc.BatchedBandSolver(nb, n, kd, chunks=16) if cfg.batch > 1 else None
     e2e_ab = bc.pinned_empty((nb, ld * n))
     e2e_b = bc.pinned_empty((nb, n))
     e2e_times = []

@@ -339,14 +339,17 @@ class BatchedBandSolver:
 
     `factor_solve(ab_host, b_host)` copies the batch in, factors every matrix and
     solves its system (bcg_dpbsv_batched), and copies L and x back into the same
-    host arrays, pipelined over `chunks` so the host<->device copies of one chunk
-    overlap the kernel of the next.  Host arrays from `pinned_empty` give
-    asynchronous copies.  Raises NotPositiveDefinite (with `.matrix`) after the
-    whole batch completes if any matrix failed.
+    host arrays.  Three streams form a pipeline over `chunks` slices of the batch:
+    host->device copies run back to back on one copy stream, each chunk's kernel starts
+    when its slice has landed, and device->host copies drain on a third stream, so both
+    PCIe directions stay busy and only the last chunk's kernel and read-back are
+    exposed.  Host arrays from `pinned_empty` give asynchronous copies.  Raises
+    NotPositiveDefinite (with `.matrix`) after the whole batch completes if any
+    matrix failed.
     """
 
     def __init__(self, batch: int, dim: int, bandwidth: int, lead_dim: int | None = None,
-                 chunks: int = 4):
+                 chunks: int = 16):
         torch = _torch()
         self.torch = torch
         self.batch, self.n, self.kd = int(batch), int(dim), int(bandwidth)
@@ -355,7 +358,7 @@ class BatchedBandSolver:
         self.ab = torch.empty((self.batch, self.ld * self.n), dtype=torch.float64, device="cuda")
         self.b = torch.empty((self.batch, self.n), dtype=torch.float64, device="cuda")
         self.info = torch.zeros(self.batch, dtype=torch.int32, device="cuda")
-        self.streams = [torch.cuda.Stream() for _ in range(2)]
+        self.h2d, self.comp, self.d2h = (torch.cuda.Stream() for _ in range(3))
         bounds = np.linspace(0, self.batch, self.chunks + 1).astype(int)
         self.ranges = [(int(bounds[i]), int(bounds[i + 1])) for i in range(self.chunks)
                        if bounds[i + 1] > bounds[i]]
@@ -369,19 +372,31 @@ class BatchedBandSolver:
         ta = torch.from_numpy(a)
         tb = torch.from_numpy(b_host)
         cur = torch.cuda.current_stream()
-        for s in self.streams:
+        for s in (self.h2d, self.comp, self.d2h):
             s.wait_stream(cur)
-        for idx, (lo, hi) in enumerate(self.ranges):
-            st = self.streams[idx % 2]
-            with torch.cuda.stream(st):
+        landed, done = [], []
+        with torch.cuda.stream(self.h2d):
+            for lo, hi in self.ranges:
                 self.ab[lo:hi].copy_(ta[lo:hi], non_blocking=True)
                 self.b[lo:hi].copy_(tb[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.h2d)
+                landed.append(ev)
+        with torch.cuda.stream(self.comp):
+            for (lo, hi), ev in zip(self.ranges, landed):
+                self.comp.wait_event(ev)
                 dpbsv_batched_device(self.ab[lo:hi], self.n, self.kd, self.ld, self.b[lo:hi], hi - lo,
-                                     info=self.info[lo:hi], stream=st)
+                                     info=self.info[lo:hi], stream=self.comp)
                 self.launches += 1
+                e2 = torch.cuda.Event()
+                e2.record(self.comp)
+                done.append(e2)
+        with torch.cuda.stream(self.d2h):
+            for (lo, hi), ev in zip(self.ranges, done):
+                self.d2h.wait_event(ev)
                 ta[lo:hi].copy_(self.ab[lo:hi], non_blocking=True)
                 tb[lo:hi].copy_(self.b[lo:hi], non_blocking=True)
-        for s in self.streams:
+        for s in (self.h2d, self.comp, self.d2h):
             cur.wait_stream(s)
         info = self.info.cpu().numpy()  # synchronises
         if check:
