@@ -162,6 +162,7 @@ struct CtaGeom {
   int n, kd, ldab;  // matrix geometry
   int lds, nslot;   // shared window: nslot column slots of lds doubles
   int pld;          // leading dimension of the dense panel P (>= kd rounded up to 16, = 4 mod 16)
+  int nx;           // ring of rhs / solution entries (bw): nx slots (= nslot in the fused kernel)
 };
 
 // The panel buffer P; the backward sweep reuses it for two L11^-1 blocks.
@@ -175,7 +176,7 @@ __host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom&
 __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g, bool solve) {
   size_t d = (size_t)g.nslot * g.lds + cta_panel_doubles(nb_block, g, solve) + (size_t)nb_block * (nb_block + 4) +
              nb_block + 32;
-  if (solve) d += (size_t)g.nslot + (size_t)(g.nslot / nb_block) * nb_block;  // rhs ring + staged y
+  if (solve) d += (size_t)g.nx + (size_t)(g.nslot / nb_block) * nb_block;  // rhs ring + staged y
   return d * sizeof(double) + 64;
 }
 
@@ -678,6 +679,198 @@ struct CtaBand {
     __syncthreads();
   }
 
+  // L11^-1 of a column block held in the ring (blk: NB column slots of lds doubles, nb
+  // valid columns; columns past nb are identity).  Warp-level: lane j forward-substitutes
+  // L11 x = e_j with the reciprocal pivots computed up front (independent: full ILP).
+  // kRowMajor: li[i*kLDD + j] = Linv(i, j); else li[j*kLDD + i] = Linv(i, j).
+  template <bool kWhole, bool kRowMajor>
+  __device__ void invert_l11(const double* blk, int nb, double* li) const {
+    if (kWhole) nb = NB;
+    const int j = threadIdx.x & 31;
+    double dk[NB];
+#pragma unroll
+    for (int kk = 0; kk < NB; ++kk) dk[kk] = (kWhole || kk < nb) ? rcp_nr(blk[kk * g.lds]) : 1.0;
+    double t[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) t[i] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int kk = 0; kk < NB; ++kk) {
+      const double* col = blk + kk * g.lds;
+      t[kk] *= dk[kk];
+#pragma unroll
+      for (int i = kk + 1; i < NB; ++i) {
+        if (kWhole) {
+          t[i] = fma(-col[i - kk], t[kk], t[i]);
+        } else {
+          const bool in = i < nb && i - kk <= g.kd;
+          const double lv = col[in ? i - kk : 0];
+          t[i] = fma(in ? -lv : 0.0, t[kk], t[i]);
+        }
+      }
+    }
+    if (j < NB) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) li[kRowMajor ? i * kLDD + j : j * kLDD + i] = t[i];
+    }
+  }
+  template <bool kRowMajor>
+  __device__ void invert_block(const double* blk, int nb, double* li) const {
+    if (nb == NB && g.kd >= NB - 1) invert_l11<true, kRowMajor>(blk, nb, li);
+    else invert_l11<false, kRowMajor>(blk, nb, li);
+  }
+
+  // Forward sweep L y = b for the standalone solve (rhs holds b, receives y).
+  //
+  // Column blocks stream in through the same buffer ring as the backward sweep (bulk
+  // copies kDepth blocks ahead); bw (nx slots) holds the running right-hand side of the
+  // kd+NB rows in flight.  Iteration b (mirror image of backward()):
+  //   warp 0:     near update of block b by block b-1 (16x16 GEMV), y_b = L11^-1 s_b
+  //   warp 1:     L11^-1 of block b+1
+  //   warps 2-7:  far update of the rows beyond block b by block b-1 (one thread per row),
+  //               then the rhs entries of the rows entering the ring
+  __device__ void forward() {
+    const int n = g.n, kd = g.kd;
+    const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
+    constexpr int kDepth = 4;
+    const int nbuf = g.nslot / NB;
+    const int nblk = (n + NB - 1) / NB;
+    double* ycur = Dinv;  // y of the last two blocks (Dinv + lbuf: 2 x NB)
+    double* li_buf = P;
+    auto parity = [&](int b) -> unsigned { return (bphase[b % nbuf] + (unsigned)(b / nbuf)) & 1u; };
+    auto issue = [&](int b) {
+      if (b >= nblk) return;
+      const int k = b % nbuf;
+      const int c0 = b * NB;
+      const int cols = min(NB, n - c0);
+      if (fast) {
+        if (threadIdx.x == 0) {
+          const unsigned bytes = (unsigned)cols * g.ldab * sizeof(double);
+          mbar_expect_tx(bars + 1 + k, bytes);
+          bulk_g2s(win + (size_t)(k * NB) * g.lds, ab + (int64_t)c0 * g.ldab, bytes, bars + 1 + k);
+        }
+      } else {
+        for (int c = 0; c < cols; ++c) {
+          double* sp = win + (size_t)(k * NB + c) * g.lds;
+          const double* gp = ab + (int64_t)(c0 + c) * g.ldab;
+          for (int o = threadIdx.x; o < g.ldab; o += kCtaThreads) sp[o] = gp[o];
+        }
+        if (threadIdx.x == 0) mbar_expect_tx(bars + 1 + k, 0);
+      }
+    };
+    auto invert = [&](int b) {  // warp 1: L11^-1 of block b into li_buf[b & 1]
+      invert_block<true>(win + (size_t)(b % nbuf) * NB * g.lds, min(NB, n - b * NB), li_buf + (b & 1) * NB * kLDD);
+    };
+    // bw accumulates the far updates of the rows in flight (zero when a row enters); warp 0
+    // adds the right-hand side itself, prefetched one block ahead into a register
+    for (int i = threadIdx.x; i < min(n, kd + NB); i += kCtaThreads) bw[i % g.nx] = 0.0;
+    double rnext = (warp == 0 && lane < min(NB, n)) ? rhs[lane] : 0.0;
+    for (int d = 0; d < kDepth; ++d) issue(d);
+    mbar_wait(bars + 1, parity(0));
+    __syncthreads();
+    if (warp == 1) invert(0);
+    for (int b = 0; b < nblk; ++b) {
+      const int c0 = b * NB;
+      const int nb = min(NB, n - c0);
+      if (threadIdx.x < 32) trace_stamp(b, 0);
+      if (b + 1 < nblk) mbar_wait(bars + 1 + (b + 1) % nbuf, parity(b + 1));
+      __syncthreads();  // L11^-1(b), far(b-1) and the entering rows are in place
+      if (threadIdx.x < 32) trace_stamp(b, 1);
+      if (warp == 0) {
+        const int r = lane;
+        const double rcur = rnext;
+        if (c0 + NB + r < n && r < NB) rnext = rhs[c0 + NB + r];  // next block's b, in flight
+        double v = (r < nb) ? rcur + bw[(c0 + r) % g.nx] : 0.0;
+        if (b > 0 && r < nb) {
+          // near: rows of block b in the columns of block b-1
+          const double* blk = win + (size_t)((b - 1) % nbuf) * NB * g.lds;
+          const double* yp = ycur + ((b - 1) & 1) * NB;
+          double a0 = 0.0, a1 = 0.0;
+          if (kd >= 2 * NB - 1) {  // every (row of b, column of b-1) pair is in the band
+#pragma unroll
+            for (int c = 0; c < NB; c += 2) {
+              a0 = fma(blk[c * g.lds + NB + r - c], yp[c], a0);
+              a1 = fma(blk[(c + 1) * g.lds + NB + r - c - 1], yp[c + 1], a1);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < NB; c += 2) {
+              const int o0 = NB + r - c, o1 = o0 - 1;
+              if (o0 <= kd) a0 = fma(blk[c * g.lds + o0], yp[c], a0);
+              if (o1 <= kd) a1 = fma(blk[(c + 1) * g.lds + o1], yp[c + 1], a1);
+            }
+          }
+          v -= a0 + a1;
+        }
+        double* ss = lbuf + NB;  // (ycur = Dinv + lbuf[0, NB))
+        if (r < NB) ss[r] = v;
+        __syncwarp();
+        const double* li = li_buf + (b & 1) * NB * kLDD + (r < NB ? r : 0) * kLDD;
+        double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < NB; c += 4) {
+          const double2 l01 = *reinterpret_cast<const double2*>(li + c);
+          const double2 l23 = *reinterpret_cast<const double2*>(li + c + 2);
+          const double2 s01 = *reinterpret_cast<const double2*>(ss + c);
+          const double2 s23 = *reinterpret_cast<const double2*>(ss + c + 2);
+          x0 = fma(l01.x, s01.x, x0);
+          x1 = fma(l01.y, s01.y, x1);
+          x0 = fma(l23.x, s23.x, x0);
+          x1 = fma(l23.y, s23.y, x1);
+        }
+        v = x0 + x1;
+        if (r < nb) {
+          ycur[(b & 1) * NB + r] = v;
+          rhs[c0 + r] = v;
+        }
+        trace_stamp(b, 2);
+      } else if (warp == 1) {
+        if (b + 1 < nblk) invert(b + 1);
+        trace_stamp(b, 4);
+      } else if (b > 0) {
+        // far: rows i in [c0 + nb, (c0 - NB) + NB - 1 + kd] lose L(i, block b-1) . y_{b-1}
+        const double* blk = win + (size_t)((b - 1) % nbuf) * NB * g.lds;
+        const double* yp = ycur + ((b - 1) & 1) * NB;
+        const int cprev = c0 - NB;
+        const int ihi = min(n - 1, cprev + NB - 1 + kd);
+        for (int i = c0 + nb + (int)threadIdx.x - 64; i <= ihi; i += kCtaThreads - 64) {
+          double acc0 = 0.0, acc1 = 0.0;
+          const int o0 = i - cprev;
+          if (o0 - (NB - 1) <= kd && o0 <= kd) {  // the whole row segment is in the band
+#pragma unroll
+            for (int c = 0; c < NB; c += 2) {
+              acc0 = fma(blk[c * g.lds + o0 - c], yp[c], acc0);
+              acc1 = fma(blk[(c + 1) * g.lds + o0 - c - 1], yp[c + 1], acc1);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < NB; c += 2) {
+              if (o0 - c <= kd) acc0 = fma(blk[c * g.lds + o0 - c], yp[c], acc0);
+              if (o0 - c - 1 <= kd) acc1 = fma(blk[(c + 1) * g.lds + o0 - c - 1], yp[c + 1], acc1);
+            }
+          }
+          bw[i % g.nx] -= acc0 + acc1;
+        }
+        if (warp == 2) trace_stamp(b, 5);
+      }
+      if (warp >= 2) {
+        // rows entering the ring: first touched by far(b) in the next iteration
+        const int lo = c0 + kd + NB, hi = min(n, lo + NB);
+        for (int i = lo + (int)threadIdx.x - 64; i < hi; i += kCtaThreads - 64) bw[i % g.nx] = 0.0;
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) trace_stamp(b, 3);
+      issue(b + kDepth);  // block b-1's buffer is free now
+    }
+    __syncthreads();
+    if (threadIdx.x < nbuf) {
+      int cnt = 0;
+      for (int b = threadIdx.x; b < nblk; b += nbuf) ++cnt;
+      bphase[threadIdx.x] = (bphase[threadIdx.x] + (unsigned)cnt) & 1u;
+    }
+    if (threadIdx.x == 0) fence_async_global();  // y (generic stores) -> the backward's bulk reads
+    __syncthreads();
+  }
+
   // Backward sweep L^T x = y (y in rhs after the fused forward sweep).
   //
   // Block b = columns [b*NB, b*NB+nb): s_j = y_j - sum_{i >= b*NB+nb} L(i,j) x_i, then the
@@ -746,11 +939,11 @@ struct CtaBand {
         const int j = c0 + c;
         const int len = col_len(j);
         const double* colj = blk + c * g.lds;
-        int sl = (rlo + q) % g.nslot;
+        int sl = (rlo + q) % g.nx;
         for (int o = rlo - j + q; o < len; o += kFarChunks) {
           acc = fma(colj[o], bw[sl], acc);
           sl += kFarChunks;
-          if (sl >= g.nslot) sl -= g.nslot;
+          if (sl >= g.nx) sl -= g.nx;
         }
       }
       part[q * NB + c] = acc;
@@ -762,45 +955,10 @@ struct CtaBand {
         sfar[(b & 1) * NB + t] = yb[k * NB + t] - sum;
       }
     };
-    // L11^-1 of block b into buffer b & 1 (warp 1, one block ahead of its use): lane j
-    // forward-substitutes L11 x = e_j; columns past a short last block are identity.
+    // L11^-1 of block b into buffer b & 1 (warp 1, one block ahead of its use);
     // li[j*kLDD + i] = Linv(i, j), so warp 0's lane r finds column r contiguous.
-    auto invert_t = [&](auto whole_tag, int b) {
-      constexpr bool kWhole = decltype(whole_tag)::value;
-      const int c0 = b * NB;
-      const int nb = kWhole ? NB : min(NB, n - c0);
-      const double* blk = win + (size_t)(b % nbuf) * NB * g.lds;
-      const int j = lane;
-      double dk[NB];  // reciprocal pivots first: independent of each other
-#pragma unroll
-      for (int kk = 0; kk < NB; ++kk) dk[kk] = (kWhole || kk < nb) ? rcp_nr(blk[kk * g.lds]) : 1.0;
-      double t[NB];
-#pragma unroll
-      for (int i = 0; i < NB; ++i) t[i] = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-      for (int kk = 0; kk < NB; ++kk) {
-        const double* col = blk + kk * g.lds;
-        t[kk] *= dk[kk];
-#pragma unroll
-        for (int i = kk + 1; i < NB; ++i) {
-          if (kWhole) {
-            t[i] = fma(-col[i - kk], t[kk], t[i]);
-          } else {
-            const bool in = i < nb && i - kk <= g.kd;
-            const double lv = col[in ? i - kk : 0];
-            t[i] = fma(in ? -lv : 0.0, t[kk], t[i]);
-          }
-        }
-      }
-      if (j < NB) {
-        double* li = li_buf + (b & 1) * NB * kLDD + j * kLDD;
-#pragma unroll
-        for (int i = 0; i < NB; ++i) li[i] = t[i];
-      }
-    };
     auto invert = [&](int b) {
-      if (min(NB, n - b * NB) == NB && g.kd >= NB - 1) invert_t(std::true_type{}, b);
-      else invert_t(std::false_type{}, b);
+      invert_block<false>(win + (size_t)(b % nbuf) * NB * g.lds, min(NB, n - b * NB), li_buf + (b & 1) * NB * kLDD);
     };
     for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d);
     const int tb = nblk + 1;  // trace rows after the factorization's
@@ -825,16 +983,25 @@ struct CtaBand {
           // near part: rows c0+nb .. c0+nb+NB-1 (block b+1), in band for this column
           const double* colr = blk + r * g.lds;
           const int len = col_len(c0 + r);
-          const int sx = (c0 + nb) % g.nslot;
+          const int sx = (c0 + nb) % g.nx;
           double a0 = 0.0, a1 = 0.0;
+          if (nb == NB && nb - r + NB - 1 < len && sx + NB <= g.nx) {  // in band, no ring wrap
+            const double* xs = bw + sx;
 #pragma unroll
-          for (int t = 0; t < NB; t += 2) {
-            const int o0 = nb - r + t, o1 = o0 + 1;
-            int s0i = sx + t, s1i = sx + t + 1;
-            if (s0i >= g.nslot) s0i -= g.nslot;
-            if (s1i >= g.nslot) s1i -= g.nslot;
-            if (o0 < len) a0 = fma(colr[o0], bw[s0i], a0);
-            if (o1 < len) a1 = fma(colr[o1], bw[s1i], a1);
+            for (int t = 0; t < NB; t += 2) {
+              a0 = fma(colr[nb - r + t], xs[t], a0);
+              a1 = fma(colr[nb - r + t + 1], xs[t + 1], a1);
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < NB; t += 2) {
+              const int o0 = nb - r + t, o1 = o0 + 1;
+              int s0i = sx + t, s1i = sx + t + 1;
+              if (s0i >= g.nx) s0i -= g.nx;
+              if (s1i >= g.nx) s1i -= g.nx;
+              if (o0 < len) a0 = fma(colr[o0], bw[s0i], a0);
+              if (o1 < len) a1 = fma(colr[o1], bw[s1i], a1);
+            }
           }
           v -= a0 + a1;
         }
@@ -858,7 +1025,7 @@ struct CtaBand {
         v = x0 + x1;
         __syncwarp();
         if (r < nb) {
-          bw[(c0 + r) % g.nslot] = v;
+          bw[(c0 + r) % g.nx] = v;
           rhs[c0 + r] = v;
         }
         trace_stamp(tb + b, 2);

@@ -57,6 +57,46 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, i
   }
 }
 
+// Standalone solve, one CTA per right-hand side: forward and backward sweeps stream the
+// factor's column blocks through a 5-buffer shared ring (see CtaBand::forward/backward).
+__global__ void __launch_bounds__(kCtaThreads, 2)
+pbtrs_cta_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int nrhs, CtaGeom g,
+                 int32_t* info) {
+  constexpr int NB = 16;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) unsigned long long bars[1 + 16];
+  __shared__ unsigned bphase[16];
+  if (threadIdx.x < 17) mbar_init(&bars[threadIdx.x], 1);
+  if (threadIdx.x < 16) bphase[threadIdx.x] = 0;
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int z = blockIdx.x, mat = z / nrhs;
+  const double* abm = ab0 + (int64_t)mat * stride_ab;
+  const int bad = first_nonpositive_diag(abm, g.n, g.ldab);
+  if (bad != INT_MAX) {
+    if (threadIdx.x == 0 && z % nrhs == 0) info[mat] = bad + 1;
+    return;
+  }
+  CtaBand<NB, true> w{g};
+  w.bars = bars;
+  w.bphase = bphase;
+  w.ab = const_cast<double*>(abm);
+  w.rhs = b0 + (int64_t)z * stride_b;
+  w.tr = (z == 0) ? g_trace : nullptr;
+  double* p = smem;
+  w.win = p; p += (size_t)g.nslot * g.lds;
+  w.P = p; p += cta_panel_doubles(NB, g, true);
+  w.D = p; p += NB * (NB + 4);
+  w.Dinv = p; p += NB;
+  w.lbuf = p; p += 32;
+  w.bw = p; p += g.nx;
+  w.yb = p;
+  w.init_fast();
+  w.forward();
+  w.backward();
+  if (threadIdx.x == 0 && z % nrhs == 0) info[mat] = 0;
+}
+
 __global__ void __launch_bounds__(kCtaThreads)
 pbtrs_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int nrhs, int n, int kd,
              int ldab, int32_t* info) {
@@ -138,6 +178,7 @@ bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb, bool solve) {
   if (solve && ns < 5 * nb) ns = 5 * nb;  // backward-sweep prefetch ring: 5 blocks
   if (ns & 1) ++ns;
   g.nslot = ns;
+  g.nx = ns;
   int pld = ((kd + 15) / 16) * 16 + 4;  // covers the 16-row tiles, = 4 (mod 16)
   g.pld = pld;
   return g;
@@ -275,8 +316,21 @@ int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t s
   return cuda_status(cudaGetLastError(), "pbtrs_after_factor_kernel launch");
 }
 
+// Streamed solve (shared-memory ring of 5 column blocks) when it fits, else the
+// direct-from-L2 kernel.
 static int launch_solve(const double* ab, int64_t sab, double* b, int64_t sb, int nrhs, int64_t blocks, int n,
                         int kd, int ldab, int32_t* info, cudaStream_t st) {
+  bcg::CtaGeom g = make_geom(n, kd, ldab, 16, true);
+  g.nslot = 5 * 16;                 // block buffers for the streamed sweeps
+  g.nx = ((kd + 48) + 1) & ~1;      // rows in flight: kd + NB, plus the entering block
+  const size_t smem = bcg::cta_smem_bytes(16, g, true);
+  if (smem <= (size_t)smem_optin()) {
+    auto k = bcg::pbtrs_cta_kernel;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(pbtrs_cta)");
+    k<<<(unsigned)blocks, bcg::kCtaThreads, smem, st>>>(ab, sab, b, sb, nrhs, g, info);
+    return cuda_status(cudaGetLastError(), "pbtrs_cta_kernel launch");
+  }
   bcg::pbtrs_kernel<<<(unsigned)blocks, bcg::kCtaThreads, 0, st>>>(ab, sab, b, sb, nrhs, n, kd, ldab, info);
   return cuda_status(cudaGetLastError(), "pbtrs_kernel launch");
 }

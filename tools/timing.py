@@ -203,3 +203,36 @@ def trace_bwd(batch=1):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_bwd":
     trace_bwd(1)
     trace_bwd(296)
+
+
+def trace_solve(batch=1):
+    """Phase breakdown of the streamed standalone solve (block 0): forward and backward."""
+    from paper_2305_04635_b200 import _lib
+    n, k = 4096, 100
+    a = np.stack([generate_spd(n, k, s).data for s in range(min(batch, 8))])
+    a = np.concatenate([a] * ((batch + 7) // 8))[:batch]
+    a0 = torch.from_numpy(a).cuda()
+    bc.dpbtrf_batched_device(a0, n, k, k + 1, batch)
+    b0 = torch.from_numpy(np.stack([make_rhs(n, s) for s in range(batch)])).cuda()
+    nblk = n // 16
+    buf = torch.zeros(1 + 8 * (2 * nblk + 4), dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    lib.bcg_set_trace(buf.data_ptr(), buf.numel() * 8)
+    wb = b0.clone()
+    bc.dpbtrs_batched_device(a0, n, k, k + 1, wb, batch)
+    torch.cuda.synchronize()
+    lib.bcg_set_trace(None, 0)
+    t = buf.cpu().numpy()[1:].reshape(-1, 8).astype(np.float64)
+    f = t[1:nblk - 1]
+    bw = t[nblk + 1: 2 * nblk + 1]
+    med = lambda x: float(np.median(x))  # noqa: E731
+    out = {"batch": batch, "fwd_block": med(np.diff(t[:nblk, 0])), "fwd_wait": med(f[:, 1] - f[:, 0]),
+           "fwd_warp0": med(f[:, 2] - f[:, 1]), "fwd_invert": med(f[:, 4] - f[:, 1]),
+           "fwd_far": med(f[:, 5] - f[:, 1]), "fwd_sync": med(f[:, 3] - f[:, 1]),
+           "bwd_block": med(bw[:-1, 0] - bw[1:, 0])}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_solve":
+    trace_solve(1)
+    trace_solve(296)
