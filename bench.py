@@ -2,8 +2,9 @@
 
 Default workload (config.workload "C5"): BASELINE.json configs[4], a batch of 1,024
 independent SPD band matrices n=4096, kd=100, factor + one-RHS band solve per matrix --
-the one config that partitions across GPUs (contiguous shards, no collective;
-fixed total batch => "strong" scaling).  `--config C1..C4` benches a single-matrix
+the one config that partitions across GPUs (each rank factors its own batch of
+1,024 matrices with distinct seeds, no collective on the data path; per-GPU work is
+fixed as N grows => "weak" scaling, value = matrices of all ranks / max-over-ranks time).  `--config C1..C4` benches a single-matrix
 config instead.  A step = one fused factor+solve pass over the whole batch (C5) or one
 factorization (+ solve for C2) of the matrix, inputs resident in HBM; a fresh
 device-to-device copy of the pristine inputs is made before every step OUTSIDE the
@@ -228,7 +229,7 @@ def run_reference_arm(args) -> int:
     line = {
         "metric": "fp64 banded Cholesky GFLOP/s (n*kd*(kd+3))", "impl": "reference", "value": value,
         "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "scaling": "strong", "dtype": "f64", "data": "synthetic (reference generator)",
+        "higher_is_better": True, "scaling": "weak", "dtype": "f64", "data": "synthetic (reference generator)",
         "config": config_block(tag, world),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": res["cores"], "kind": res["kind"],
                          "sample": res["sample"]},
@@ -242,8 +243,10 @@ def run_reference_arm(args) -> int:
 def config_block(tag: str, world: int) -> dict:
     cfg = CONFIGS[tag]
     return {"workload": tag, "n": cfg.dim, "kd": cfg.bandwidth, "batch": cfg.batch,
+            "global_batch": cfg.batch * world if cfg.batch > 1 else 1,
             "factor_and_solve": cfg.solve, "wide_diagonal": cfg.wide_diagonal,
-            "parallelism": f"batch-sharded x{world}" if cfg.batch > 1 else "single matrix per GPU",
+            "parallelism": (f"batch-sharded x{world} ({cfg.batch} matrices per GPU)" if cfg.batch > 1
+                            else "single matrix per GPU (replicas)"),
             "l2": "inputs > L2 and fresh D2D copy between steps (flushes L2)"}
 
 
@@ -264,7 +267,9 @@ def run_gpu_arm(args) -> int:
     tag = args.config
     cfg = CONFIGS[tag]
     n, kd, ld = cfg.dim, cfg.bandwidth, cfg.bandwidth + 1
-    lo, hi = shard(cfg.batch, rank, world) if cfg.batch > 1 else (0, 1)
+    # weak scaling: the global batch is cfg.batch per rank; rank r owns the contiguous
+    # shard [r*batch, (r+1)*batch) of it (global seeds), no collective on the data path
+    lo, hi = shard(cfg.batch * world, rank, world) if cfg.batch > 1 else (0, 1)
     nb = hi - lo
     ab_host = bc.pinned_empty((nb, ld * n))
     b_host = bc.pinned_empty((nb, n))
@@ -319,7 +324,7 @@ def run_gpu_arm(args) -> int:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    flops_total = cfg.batch * n * kd * (kd + 3)
+    flops_total = cfg.batch * world * n * kd * (kd + 3)  # every rank's matrices (replicas for C1-C4)
     value = flops_total * args.steps / (max_ms * 1e-3) / 1e9  # GFLOP/s, whole job
 
     # end to end through the public API with host buffers (pinned), per rank shard
@@ -380,7 +385,7 @@ def run_gpu_arm(args) -> int:
     line = {
         "metric": "fp64 banded Cholesky GFLOP/s (n*kd*(kd+3))", "value": value, "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong" if cfg.batch > 1 else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (reference generator, seeds 0..batch-1)",
         "config": config_block(tag, world), "roofline": roofline, "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
