@@ -334,7 +334,9 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         const int need = max(0, j - 1 - lo);  // worker updates m in [lo, j-2]
         if (threadIdx.x == 32) {
           bool ok = spin_ge(TC(j + 1, 1), need, ws.ctrl + 1, 64) && spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
+          trace_stamp_to(tr, j, 6);
           if (ok && has_w) ok = spin_ge(LR(j + 1, 2), 1, ws.ctrl + 1, 64);
+          trace_stamp_to(tr, j, 7);
           s_ok = ok;
         }
         named_sync(1, 224);
@@ -421,7 +423,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   double* sB = sA + E;
   double* sC = sA + 2 * E;
   const int Q = g.Q;
-  const long long total = (long long)nblk * Q;
+  const long long total = (long long)(nblk + 1) * Q;  // super-step nblk: the last rest updates
   int next_ticket = 0;
   if (kPrefetchTicket && gt == 0) next_ticket = atomicAdd(ws.ctrl, 1);
   auto gsync = [&]() { named_sync(bar, GT); };
@@ -464,9 +466,16 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
     const long long t = warp_uniform(s_task2[grp]);
     if (t >= total) break;
     ph(0);
-    const int j = (int)(t / Q), q = (int)(t - (long long)j * Q);
+    // Ticket order, super-step s (Q tickets): the TRSMs of step s, then the "rest" updates
+    // of step s-1 (tiles not feeding the next panel), then step s's updates of the tile
+    // column s+1.  Still a topological order (a TRSM of step s needs only column-s updates,
+    // handed out in super-step s-1), but the critical TRSMs no longer queue behind the
+    // previous step's far-from-diagonal updates.
+    const int sstep = (int)(t / Q), q = (int)(t - (long long)sstep * Q);
+    const int nrest = T * (T - 1) / 2;
     if (q < T - 1) {
       // TRSM: L(R, j) = A(R, j) L(j,j)^-T
+      const int j = sstep;
       const int R = j + 2 + q;
       if (R >= nblk) { gsync(); continue; }
       if (gt == 0) s_ok2[grp] = wait3(LR(j, 0), 1, TC(R, R - j), j - max(0, R - T), nullptr, 0);
@@ -486,22 +495,22 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       gpublish(LR(R, R - j), 1);
       ph(4);
     } else {
-      // update order within a step: first the tile column that feeds the next panel
-      // (S = j+1, R = j+1..j+T) -- the next step's TRSMs wait on exactly these -- then
-      // the rest row by row from the diagonal (a = R-j-1 >= 1, b = R-S < a)
+      // rest updates of step s-1 row by row from the diagonal (a = R-j-1 >= 1, b = R-S < a),
+      // then the tile column S = j+1 of step s (a = b = R-j-1)
       const int u = q - (T - 1);
-      int a, b;
-      if (u < T) {
-        a = u;
-        b = u;
+      int a, b, j;
+      if (u < nrest) {
+        j = sstep - 1;
+        a = (int)((sqrtf(8.0f * (float)u + 1.0f) + 1.0f) * 0.5f);
+        while (a * (a - 1) / 2 > u) --a;
+        while ((a + 1) * a / 2 <= u) ++a;
+        b = u - a * (a - 1) / 2;
       } else {
-        const int v = u - T;
-        a = (int)((sqrtf(8.0f * (float)v + 1.0f) + 1.0f) * 0.5f);
-        while (a * (a - 1) / 2 > v) --a;
-        while ((a + 1) * a / 2 <= v) ++a;
-        b = v - a * (a - 1) / 2;
+        j = sstep;
+        a = b = u - nrest;
       }
       const int R = j + 1 + a, S = R - b;
+      if (j < 0 || j >= nblk) { gsync(); continue; }
       const bool pivot_owned = (R == j + 1) || (R == j + 2 && S >= j + 1);
       if (R >= nblk || pivot_owned) { gsync(); continue; }
       const int done = j - max(0, R - T);

@@ -124,6 +124,8 @@ def trace(tag):
         v = d[:-1, i]
         out[nm] = float(np.median(v))
     out["gap"] = float(np.median(nxt))
+    out["wait_tc"] = float(np.median(st[:-1, 6] - st[:-1, 0]))
+    out["wait_lr"] = float(np.median(st[:-1, 7] - st[:-1, 6]))
     wk = t[-8:-3].astype(np.float64)
     if wk.sum() > 0:
         out["worker_share"] = {k: round(float(v / wk.sum()), 3)
