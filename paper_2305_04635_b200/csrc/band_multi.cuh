@@ -466,18 +466,20 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
     const long long t = warp_uniform(s_task2[grp]);
     if (t >= total) break;
     ph(0);
-    // Ticket order, super-step s (Q tickets): the TRSMs of step s, then the "rest" updates
-    // of step s-1 (tiles not feeding the next panel), then step s's updates of the tile
-    // column s+1.  Still a topological order (a TRSM of step s needs only column-s updates,
-    // handed out in super-step s-1), but the critical TRSMs no longer queue behind the
-    // previous step's far-from-diagonal updates.
+    // Ticket order, super-step s (Q tickets):
+    //   A  the updates of step s-1 to the tile column s+1 (rows s+2..),
+    //   B  the row tasks of step s: TRSM L(R,s) = A(R,s) L(s,s)^-T, then -- with L(R,s)
+    //      still in shared memory -- the update of (R, s+1), which the row's TRSM of step
+    //      s+1 waits for: one task per row per step on the critical row chain,
+    //   C  the remaining updates of step s-1 (columns s+2..).
+    // A topological order (B needs A of its super-step and B of the previous one; C needs
+    // the TRSMs of step s-1), and the critical row tasks never queue behind C.
     const int sstep = (int)(t / Q), q = (int)(t - (long long)sstep * Q);
-    const int nrest = T * (T - 1) / 2;
-    if (q < T - 1) {
-      // TRSM: L(R, j) = A(R, j) L(j,j)^-T
+    const int nA = T - 1, nB = T - 1;
+    if (q >= nA && q < nA + nB) {
       const int j = sstep;
-      const int R = j + 2 + q;
-      if (R >= nblk) { gsync(); continue; }
+      const int R = j + 2 + (q - nA);
+      if (R >= nblk || j >= nblk) { gsync(); continue; }
       if (gt == 0) s_ok2[grp] = wait3(LR(j, 0), 1, TC(R, R - j), j - max(0, R - T), nullptr, 0);
       gsync();
       if (!warp_uniform(s_ok2[grp])) break;
@@ -494,20 +496,38 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       ph(3);
       gpublish(LR(R, R - j), 1);
       ph(4);
+      // the row's update of tile (R, j+1) ((j+2, j+1) is the pivot's)
+      const int S = j + 1;
+      if (R >= j + 3 && S < nblk) {
+        const int done = j - max(0, R - T);
+        if (gt == 0) s_ok2[grp] = wait3(LR(S, 1), 1, TC(R, R - S), done, nullptr, 0);
+        gsync();
+        if (!warp_uniform(s_ok2[grp])) break;
+        ph(1);
+        load_tile<NB, GT>(sB, ab, g, S, j, gt);
+        load_tile<NB, GT>(sC, ab, g, R, S, gt);
+        gsync();
+        ph(2);
+        tile_gemm<NB, true, GW>(sC, sA, sB, wg, bar, GT);
+        store_tile<NB, GT>(sC, ab, g, R, S, gt);
+        ph(3);
+        gpublish(TC(R, R - S), done + 1);
+        ph(4);
+      }
     } else {
-      // rest updates of step s-1 row by row from the diagonal (a = R-j-1 >= 1, b = R-S < a),
-      // then the tile column S = j+1 of step s (a = b = R-j-1)
-      const int u = q - (T - 1);
-      int a, b, j;
-      if (u < nrest) {
-        j = sstep - 1;
-        a = (int)((sqrtf(8.0f * (float)u + 1.0f) + 1.0f) * 0.5f);
-        while (a * (a - 1) / 2 > u) --a;
-        while ((a + 1) * a / 2 <= u) ++a;
-        b = u - a * (a - 1) / 2;
+      // updates of step s-1: part A (b = a-1: column s+1) or part C (b <= a-2)
+      const int j = sstep - 1;
+      int a, b;
+      if (q < nA) {
+        a = q + 1;
+        b = a - 1;
       } else {
-        j = sstep;
-        a = b = u - nrest;
+        const int v = q - nA - nB;
+        int w = (int)((1.0f + sqrtf(8.0f * (float)v + 1.0f)) * 0.5f);
+        while (w * (w - 1) / 2 > v) --w;
+        while ((w + 1) * w / 2 <= v) ++w;
+        a = w + 1;
+        b = v - w * (w - 1) / 2;
       }
       const int R = j + 1 + a, S = R - b;
       if (j < 0 || j >= nblk) { gsync(); continue; }
@@ -550,7 +570,7 @@ inline MultiGeom multi_geom(int n, int kd, int ldab) {
   g.ldab = ldab;
   g.nblk = (n + kMultiNB - 1) / kMultiNB;
   g.T = (kd + kMultiNB - 1) / kMultiNB;
-  g.Q = (g.T - 1) + g.T * (g.T + 1) / 2;
+  g.Q = (g.T - 1) + g.T * (g.T - 1) / 2;  // per super-step: T-1 row tasks + the step's other updates
   return g;
 }
 
