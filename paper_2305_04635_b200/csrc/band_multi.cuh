@@ -38,6 +38,10 @@
 namespace bcg {
 
 constexpr int kMultiThreads = 256;
+#ifndef BCG_WIDE_GROUPS
+#define BCG_WIDE_GROUPS 4  // worker groups per CTA for wide bands (kd >= 1000)
+#define BCG_WIDE_PERSM 2
+#endif
 #ifndef BCG_MULTI_PREFETCH
 #define BCG_MULTI_PREFETCH false  // fetch a worker's next ticket while its current task runs
 #endif
@@ -157,7 +161,7 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
                                           int bar_id = 0, int bar_cnt = kMultiThreads) {
   constexpr int LD = MultiTile<NB>::LD;
   constexpr int MT = NB / 8;
-  constexpr int WM = (NB == 64) ? 2 : 4;  // warps along m
+  constexpr int WM = (NB == 64) ? 2 : (NW < 4 ? NW : 4);  // warps along m
   constexpr int WN = NW / WM;
   constexpr int TM = MT / WM, TN = MT / WN;
   static_assert(TM >= 1 && TN >= 1, "tile too small for the warps");
@@ -417,8 +421,8 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   constexpr bool kPrefetchTicket = BCG_MULTI_PREFETCH;
   const int grp = warp / GW, gt = threadIdx.x - grp * GT, wg = warp - grp * GW;
   const int bar = 1 + grp;
-  __shared__ int s_task2[2], s_ok2[2];
-  __shared__ double sdinv2[2][NB];
+  __shared__ int s_task2[kGroups], s_ok2[kGroups];
+  __shared__ double sdinv2[kGroups][NB];
   double* sA = smem + grp * 3 * E;
   double* sB = sA + E;
   double* sC = sA + 2 * E;
@@ -619,7 +623,7 @@ inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, vo
 
 inline int launch_multi(double* ab, int n, int kd, int ldab, int32_t* info, void* workspace, int sms,
                         cudaStream_t st, char* err, size_t errlen) {
-  if (kd >= 1000) return launch_multi_t<3, 2>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
+  if (kd >= 1000) return launch_multi_t<BCG_WIDE_PERSM, BCG_WIDE_GROUPS>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
   return launch_multi_t<2, 1>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
 }
 
