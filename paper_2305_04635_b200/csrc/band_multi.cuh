@@ -98,13 +98,13 @@ __device__ __forceinline__ bool spin_ge(const int* flag, int target, const int* 
   }
 }
 
-// all threads: publish after this CTA's global stores
+// all threads: publish after this CTA's global stores.  The barrier orders every
+// thread's stores before thread 0's release, and a release is cumulative over what its
+// thread has synchronised with, so no separate fence is needed (the consumer pairs it
+// with ld.acquire + a barrier).
 __device__ __forceinline__ void cta_publish(int* flag, int value) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(flag, value);
-  }
+  if (threadIdx.x == 0) st_release(flag, value);
 }
 
 __device__ __forceinline__ void named_sync(int id, int cnt) {
@@ -433,10 +433,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   auto gsync = [&]() { named_sync(bar, GT); };
   auto gpublish = [&](int* flag, int value) {
     gsync();
-    if (gt == 0) {
-      __threadfence();
-      st_release(flag, value);
-    }
+    if (gt == 0) st_release(flag, value);  // cumulative release after the group barrier
   };
   // one thread: wait for up to three flags (issued together, then spun on one by one)
   auto wait3 = [&](const int* f0, int v0, const int* f1, int v1, const int* f2, int v2) -> bool {
