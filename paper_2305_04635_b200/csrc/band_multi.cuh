@@ -42,6 +42,10 @@ constexpr int kMultiThreads = 256;
 #define BCG_WIDE_GROUPS 4  // worker groups per CTA for wide bands (kd >= 1000)
 #define BCG_WIDE_PERSM 2
 #endif
+#ifndef BCG_WORKER_SPIN_NS
+#define BCG_WORKER_SPIN_NS 64
+#endif
+constexpr unsigned kWorkerSpinNs = BCG_WORKER_SPIN_NS;  // longest back-off of a worker's flag spin
 #ifndef BCG_MULTI_PREFETCH
 #define BCG_MULTI_PREFETCH false  // fetch a worker's next ticket while its current task runs
 #endif
@@ -438,9 +442,9 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   // one thread: wait for up to three flags (issued together, then spun on one by one)
   auto wait3 = [&](const int* f0, int v0, const int* f1, int v1, const int* f2, int v2) -> bool {
     const int a0 = ld_acquire(f0), a1 = f1 ? ld_acquire(f1) : v1, a2 = f2 ? ld_acquire(f2) : v2;
-    if (a0 < v0 && !spin_ge(f0, v0, ws.ctrl + 1, 256)) return false;
-    if (a1 < v1 && !spin_ge(f1, v1, ws.ctrl + 1, 256)) return false;
-    if (a2 < v2 && !spin_ge(f2, v2, ws.ctrl + 1, 256)) return false;
+    if (a0 < v0 && !spin_ge(f0, v0, ws.ctrl + 1, kWorkerSpinNs)) return false;
+    if (a1 < v1 && !spin_ge(f1, v1, ws.ctrl + 1, kWorkerSpinNs)) return false;
+    if (a2 < v2 && !spin_ge(f2, v2, ws.ctrl + 1, kWorkerSpinNs)) return false;
     return true;
   };
 #ifdef BCG_TRACE
