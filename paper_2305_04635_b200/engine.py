@@ -96,11 +96,31 @@ def _validate_grid(n: int, k: int, grid_dim) -> None:
 
 # -- device-resident primitives ---------------------------------------------------
 
+def _dev(t, torch, dtype, numel: int, name: str):
+    """Argument check for a device buffer handed to the C ABI as a raw pointer: the
+    kernels index it up to `numel`, so dtype, device, layout and size must hold."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ShapeMismatch(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ShapeMismatch(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ShapeMismatch(f"{name} must be contiguous")
+    if t.numel() < numel:
+        raise ShapeMismatch(f"{name} holds {t.numel()} elements, needs {numel}")
+    return t
+
+
+def _info(torch, info, count: int, device):
+    if info is None:
+        return torch.zeros(count, dtype=torch.int32, device=device)
+    return _dev(info, torch, torch.int32, count, "info")
+
+
 def dpbtrf_device(ab, n: int, kd: int, ldab: int, info=None, stream=None):
     """Factor one band matrix held in a CUDA float64 tensor, in place.  Returns info."""
     torch = _torch()
-    if info is None:
-        info = torch.zeros(1, dtype=torch.int32, device=ab.device)
+    _dev(ab, torch, torch.float64, ldab * n, "ab")
+    info = _info(torch, info, 1, ab.device)
     ws, need = _workspace(torch, n, kd, ldab)
     rc = _lib.load().bcg_dpbtrf(n, kd, ab.data_ptr(), ldab, info.data_ptr(),
                                 ws.data_ptr() if ws is not None else None, need,
@@ -112,8 +132,8 @@ def dpbtrf_device(ab, n: int, kd: int, ldab: int, info=None, stream=None):
 def dpbtrf_batched_device(ab, n: int, kd: int, ldab: int, batch: int, info=None, stream=None):
     """Factor `batch` matrices stored back to back (stride ldab*n) in a CUDA tensor."""
     torch = _torch()
-    if info is None:
-        info = torch.zeros(batch, dtype=torch.int32, device=ab.device)
+    _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
+    info = _info(torch, info, batch, ab.device)
     rc = _lib.load().bcg_dpbtrf_batched(n, kd, ab.data_ptr(), ldab, ldab * n, batch,
                                         info.data_ptr(), _stream_handle(torch, stream))
     _lib.check(rc, "bcg_dpbtrf_batched")
@@ -123,8 +143,9 @@ def dpbtrf_batched_device(ab, n: int, kd: int, ldab: int, batch: int, info=None,
 def dpbtrs_device(ab, n: int, kd: int, ldab: int, b, nrhs: int = 1, info=None, stream=None):
     """Solve L L^T x = b in place for nrhs right-hand sides (columns of length n)."""
     torch = _torch()
-    if info is None:
-        info = torch.zeros(1, dtype=torch.int32, device=ab.device)
+    _dev(ab, torch, torch.float64, ldab * n, "ab")
+    _dev(b, torch, torch.float64, n * nrhs, "b")
+    info = _info(torch, info, 1, ab.device)
     rc = _lib.load().bcg_dpbtrs(n, kd, ab.data_ptr(), ldab, b.data_ptr(), n, nrhs,
                                 info.data_ptr(), _stream_handle(torch, stream))
     _lib.check(rc, "bcg_dpbtrs")
@@ -132,9 +153,11 @@ def dpbtrs_device(ab, n: int, kd: int, ldab: int, b, nrhs: int = 1, info=None, s
 
 
 def dpbtrs_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=None, stream=None):
+    """Solve every system of a factored batch (L from dpbtrf_batched_device) in place in b."""
     torch = _torch()
-    if info is None:
-        info = torch.zeros(batch, dtype=torch.int32, device=ab.device)
+    _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
+    _dev(b, torch, torch.float64, n * batch, "b")
+    info = _info(torch, info, batch, ab.device)
     rc = _lib.load().bcg_dpbtrs_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
                                         batch, info.data_ptr(), _stream_handle(torch, stream))
     _lib.check(rc, "bcg_dpbtrs_batched")
@@ -144,8 +167,9 @@ def dpbtrs_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=No
 def dpbsv_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=None, stream=None):
     """Fused factor + solve of `batch` systems: ab -> L, b -> x, one launch."""
     torch = _torch()
-    if info is None:
-        info = torch.zeros(batch, dtype=torch.int32, device=ab.device)
+    _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
+    _dev(b, torch, torch.float64, n * batch, "b")
+    info = _info(torch, info, batch, ab.device)
     rc = _lib.load().bcg_dpbsv_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
                                        batch, info.data_ptr(), _stream_handle(torch, stream))
     _lib.check(rc, "bcg_dpbsv_batched")
@@ -157,8 +181,11 @@ def band_residual_device(a, l, n: int, kd: int, lda: int, ldl: int, out=None, st
     a 1-element CUDA tensor (no host synchronisation)."""
     torch = _torch()
     lib = _lib.load()
+    _dev(a, torch, torch.float64, lda * n, "a")
+    _dev(l, torch, torch.float64, ldl * n, "l")
     if out is None:
         out = torch.empty(1, dtype=torch.float64, device=a.device)
+    _dev(out, torch, torch.float64, 1, "out")
     need = int(lib.bcg_band_residual_workspace_size())
     ws = torch.empty(need // 8 + 1, dtype=torch.float64, device=a.device)
     rc = lib.bcg_band_residual(n, kd, a.data_ptr(), lda, l.data_ptr(), ldl, out.data_ptr(), ws.data_ptr(),

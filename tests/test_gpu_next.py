@@ -79,3 +79,21 @@ def test_harness_end_to_end(tmp_path):
     assert harness.parse_csv(out) == recs
     assert harness.main(["--dim", "500", "--bandwidths", "9", "--reps", "2", "--check",
                          "--out", str(tmp_path / "cli.csv")]) == 0
+
+
+def test_device_primitives_reject_bad_buffers():
+    n, k = 64, 4
+    ab = torch.zeros((k + 1) * n, dtype=torch.float64, device="cuda")
+    with pytest.raises(bc.ShapeMismatch):
+        bc.dpbtrf_device(ab[: -1], n, k, k + 1)  # too small
+    with pytest.raises(bc.ShapeMismatch):
+        bc.dpbtrf_device(ab.float(), n, k, k + 1)  # wrong dtype
+    with pytest.raises(bc.ShapeMismatch):
+        bc.dpbtrf_device(ab.cpu(), n, k, k + 1)  # host memory
+    with pytest.raises(bc.ShapeMismatch):
+        bc.dpbtrf_batched_device(ab, n, k, k + 1, 2)  # batch larger than the buffer
+    b = torch.zeros(n, dtype=torch.float64, device="cuda")
+    with pytest.raises(bc.ShapeMismatch):
+        bc.dpbtrs_device(ab, n, k, k + 1, b, nrhs=2)
+    with pytest.raises(bc.ShapeMismatch):
+        bc.dpbsv_batched_device(ab, n, k, k + 1, b, 1, info=torch.zeros(1, dtype=torch.int64, device="cuda"))
