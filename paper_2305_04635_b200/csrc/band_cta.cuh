@@ -972,8 +972,10 @@ struct CtaBand {
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
       if (threadIdx.x < 32) trace_stamp(tb + b, 0);
-      if (b >= 1) mbar_wait(bars + 1 + (b - 1) % nbuf, parity(b - 1));  // block b-1 for far(b-1)
-      __syncthreads();  // far(b) done, x of block b+1 visible
+      if (b >= 1) mbar_wait(bars + 1 + (b - 1) % nbuf, parity(b - 1));  // block b-1, per thread
+      // far(b), L11^-1(b) and x of block b+1 were published by the previous iteration's
+      // closing barrier; only the prologue's far/invert needs one here
+      if (b == nblk - 1) __syncthreads();
       if (threadIdx.x < 32) trace_stamp(tb + b, 1);
       if (warp == 0) {
         const double* blk = win + (size_t)k * NB * g.lds;
