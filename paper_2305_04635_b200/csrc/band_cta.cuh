@@ -889,15 +889,15 @@ struct CtaBand {
     const int nblk = (n + NB - 1) / NB;
     double* sfar = Dinv;            // 2 x NB: far part (incl. y) per block, double-buffered
     const bool bulk_y = fast && !(((uintptr_t)rhs) & 15);
-    // usage parity of buffer k's mbarrier for block b (blocks visit buffers in decreasing order)
-    auto parity = [&](int b) -> unsigned {
-      const int k = b % nbuf;
-      int first = nblk - 1 - ((nblk - 1 - k) % nbuf + nbuf) % nbuf;  // largest block on buffer k
-      return (bphase[k] + (unsigned)((first - b) / nbuf)) & 1u;
+    // parity of the next wait on buffer k's mbarrier, bit k (no divisions in the loop)
+    unsigned pbits = 0;
+    for (int k = 0; k < nbuf; ++k) pbits |= (bphase[k] & 1u) << k;
+    auto wait_buf = [&](int k) {
+      mbar_wait(bars + 1 + k, (pbits >> k) & 1u);
+      pbits ^= 1u << k;
     };
-    auto issue = [&](int b) {
+    auto issue = [&](int b, int k) {  // k = b % nbuf
       if (b < 0) return;
-      const int k = b % nbuf;
       const int c0 = b * NB;
       const int cols = min(NB, n - c0);
       if (fast) {
@@ -926,10 +926,9 @@ struct CtaBand {
     // far part of block b from x entries of blocks >= b+2 (warps 2-7): thread (chunk q,
     // column c) sums rows o = o_lo + q, o_lo + q + kFarChunks, ... of column c; the
     // chunk partials are added in a fixed order (deterministic) after a named barrier.
-    auto far = [&](int b) {
+    auto far = [&](int b, int k, int sx) {  // k = b % nbuf, sx = ring slot of row b*NB + nb + NB
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
-      const int k = b % nbuf;
       const double* blk = win + (size_t)k * NB * g.lds;
       const int rlo = c0 + nb + NB;  // first row of block b+2
       const int t = threadIdx.x - 64;
@@ -939,7 +938,8 @@ struct CtaBand {
         const int j = c0 + c;
         const int len = col_len(j);
         const double* colj = blk + c * g.lds;
-        int sl = (rlo + q) % g.nx;
+        int sl = sx + q;
+        if (sl >= g.nx) sl -= g.nx;
         for (int o = rlo - j + q; o < len; o += kFarChunks) {
           acc = fma(colj[o], bw[sl], acc);
           sl += kFarChunks;
@@ -957,22 +957,32 @@ struct CtaBand {
     };
     // L11^-1 of block b into buffer b & 1 (warp 1, one block ahead of its use);
     // li[j*kLDD + i] = Linv(i, j), so warp 0's lane r finds column r contiguous.
-    auto invert = [&](int b) {
-      invert_block<false>(win + (size_t)(b % nbuf) * NB * g.lds, min(NB, n - b * NB), li_buf + (b & 1) * NB * kLDD);
+    auto invert = [&](int b, int k) {
+      invert_block<false>(win + (size_t)k * NB * g.lds, min(NB, n - b * NB), li_buf + (b & 1) * NB * kLDD);
     };
-    for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d);
+    // ring positions, tracked incrementally: kb = block b's buffer, xb = ring slot of row b*NB
+    int kb = (nblk - 1) % nbuf;
+    int xb = ((nblk - 1) * NB) % g.nx;
+    auto dec = [&](int v, int by, int mod) { v -= by; return v < 0 ? v + mod : v; };
+    for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d, dec(kb, d, nbuf));
     const int tb = nblk + 1;  // trace rows after the factorization's
     // prologue: far part of the last block (nothing beyond it)
-    mbar_wait(bars + 1 + (nblk - 1) % nbuf, parity(nblk - 1));
+    wait_buf(kb);
     __syncthreads();
-    if (warp >= 2) far(nblk - 1);
-    else if (warp == 1) invert(nblk - 1);
+    if (warp >= 2) {
+      const int nbl = n - (nblk - 1) * NB;
+      int sx = xb + nbl + NB;
+      while (sx >= g.nx) sx -= g.nx;
+      far(nblk - 1, kb, sx);
+    } else if (warp == 1) {
+      invert(nblk - 1, kb);
+    }
     for (int b = nblk - 1; b >= 0; --b) {
-      const int k = b % nbuf;
+      const int k = kb, km1 = dec(kb, 1, nbuf);
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
       if (threadIdx.x < 32) trace_stamp(tb + b, 0);
-      if (b >= 1) mbar_wait(bars + 1 + (b - 1) % nbuf, parity(b - 1));  // block b-1, per thread
+      if (b >= 1) wait_buf(km1);  // block b-1, per thread
       // far(b), L11^-1(b) and x of block b+1 were published by the previous iteration's
       // closing barrier; only the prologue's far/invert needs one here
       if (b == nblk - 1) __syncthreads();
@@ -985,7 +995,8 @@ struct CtaBand {
           // near part: rows c0+nb .. c0+nb+NB-1 (block b+1), in band for this column
           const double* colr = blk + r * g.lds;
           const int len = col_len(c0 + r);
-          const int sx = (c0 + nb) % g.nx;
+          int sx = xb + nb;
+          if (sx >= g.nx) sx -= g.nx;
           double a0 = 0.0, a1 = 0.0;
           if (nb == NB && nb - r + NB - 1 < len && sx + NB <= g.nx) {  // in band, no ring wrap
             const double* xs = bw + sx;
@@ -1027,22 +1038,28 @@ struct CtaBand {
         v = x0 + x1;
         __syncwarp();
         if (r < nb) {
-          bw[(c0 + r) % g.nx] = v;
+          int sr = xb + r;
+          if (sr >= g.nx) sr -= g.nx;
+          bw[sr] = v;
           rhs[c0 + r] = v;
         }
         trace_stamp(tb + b, 2);
       } else if (b >= 1) {
         if (warp >= 2) {
-          far(b - 1);
+          int sxf = xb + NB;  // row (b-1)*NB + NB + NB = c0 + NB
+          if (sxf >= g.nx) sxf -= g.nx;
+          far(b - 1, km1, sxf);
           if (warp == 2) trace_stamp(tb + b, 5);
         } else {
-          invert(b - 1);
+          invert(b - 1, km1);
           trace_stamp(tb + b, 4);
         }
       }
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(tb + b, 3);
-      issue(b - kDepth);  // block b's buffer is free now ... and so is b+1's
+      issue(b - kDepth, dec(kb, kDepth, nbuf));  // block b+1's buffer is free now
+      kb = km1;
+      xb = dec(xb, NB, g.nx);
     }
     // buffer mbarrier phases advanced by this matrix: one completion per block
     __syncthreads();
