@@ -736,10 +736,16 @@ struct CtaBand {
     const int nblk = (n + NB - 1) / NB;
     double* ycur = Dinv;  // y of the last two blocks (Dinv + lbuf: 2 x NB)
     double* li_buf = P;
-    auto parity = [&](int b) -> unsigned { return (bphase[b % nbuf] + (unsigned)(b / nbuf)) & 1u; };
-    auto issue = [&](int b) {
+    // parity of the next wait on buffer k (bit k) and ring positions, tracked without divisions
+    unsigned pbits = 0;
+    for (int k = 0; k < nbuf; ++k) pbits |= (bphase[k] & 1u) << k;
+    auto wait_buf = [&](int k) {
+      mbar_wait(bars + 1 + k, (pbits >> k) & 1u);
+      pbits ^= 1u << k;
+    };
+    auto inc = [](int v, int by, int mod) { v += by; return v >= mod ? v - mod : v; };
+    auto issue = [&](int b, int k) {  // k = b % nbuf
       if (b >= nblk) return;
-      const int k = b % nbuf;
       const int c0 = b * NB;
       const int cols = min(NB, n - c0);
       if (fast) {
@@ -757,32 +763,34 @@ struct CtaBand {
         if (threadIdx.x == 0) mbar_expect_tx(bars + 1 + k, 0);
       }
     };
-    auto invert = [&](int b) {  // warp 1: L11^-1 of block b into li_buf[b & 1]
-      invert_block<true>(win + (size_t)(b % nbuf) * NB * g.lds, min(NB, n - b * NB), li_buf + (b & 1) * NB * kLDD);
+    auto invert = [&](int b, int k) {  // warp 1: L11^-1 of block b into li_buf[b & 1]
+      invert_block<true>(win + (size_t)k * NB * g.lds, min(NB, n - b * NB), li_buf + (b & 1) * NB * kLDD);
     };
     // bw accumulates the far updates of the rows in flight (zero when a row enters); warp 0
     // adds the right-hand side itself, prefetched one block ahead into a register
     for (int i = threadIdx.x; i < min(n, kd + NB); i += kCtaThreads) bw[i % g.nx] = 0.0;
     double rnext = (warp == 0 && lane < min(NB, n)) ? rhs[lane] : 0.0;
-    for (int d = 0; d < kDepth; ++d) issue(d);
-    mbar_wait(bars + 1, parity(0));
+    for (int d = 0; d < kDepth; ++d) issue(d, d % nbuf);
+    wait_buf(0);
     __syncthreads();
-    if (warp == 1) invert(0);
+    if (warp == 1) invert(0, 0);
+    int kb = 0, xb = 0;  // buffer of block b, ring slot of row b*NB
     for (int b = 0; b < nblk; ++b) {
+      const int kp1 = inc(kb, 1, nbuf), km1 = kb == 0 ? nbuf - 1 : kb - 1;
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
       if (threadIdx.x < 32) trace_stamp(b, 0);
-      if (b + 1 < nblk) mbar_wait(bars + 1 + (b + 1) % nbuf, parity(b + 1));
+      if (b + 1 < nblk) wait_buf(kp1);
       __syncthreads();  // L11^-1(b), far(b-1) and the entering rows are in place
       if (threadIdx.x < 32) trace_stamp(b, 1);
       if (warp == 0) {
         const int r = lane;
         const double rcur = rnext;
         if (c0 + NB + r < n && r < NB) rnext = rhs[c0 + NB + r];  // next block's b, in flight
-        double v = (r < nb) ? rcur + bw[(c0 + r) % g.nx] : 0.0;
+        double v = (r < nb) ? rcur + bw[inc(xb, r, g.nx)] : 0.0;
         if (b > 0 && r < nb) {
           // near: rows of block b in the columns of block b-1
-          const double* blk = win + (size_t)((b - 1) % nbuf) * NB * g.lds;
+          const double* blk = win + (size_t)km1 * NB * g.lds;
           const double* yp = ycur + ((b - 1) & 1) * NB;
           double a0 = 0.0, a1 = 0.0;
           if (kd >= 2 * NB - 1) {  // every (row of b, column of b-1) pair is in the band
@@ -824,11 +832,11 @@ struct CtaBand {
         }
         trace_stamp(b, 2);
       } else if (warp == 1) {
-        if (b + 1 < nblk) invert(b + 1);
+        if (b + 1 < nblk) invert(b + 1, kp1);
         trace_stamp(b, 4);
       } else if (b > 0) {
         // far: rows i in [c0 + nb, (c0 - NB) + NB - 1 + kd] lose L(i, block b-1) . y_{b-1}
-        const double* blk = win + (size_t)((b - 1) % nbuf) * NB * g.lds;
+        const double* blk = win + (size_t)km1 * NB * g.lds;
         const double* yp = ycur + ((b - 1) & 1) * NB;
         const int cprev = c0 - NB;
         const int ihi = min(n - 1, cprev + NB - 1 + kd);
@@ -859,7 +867,9 @@ struct CtaBand {
       }
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(b, 3);
-      issue(b + kDepth);  // block b-1's buffer is free now
+      issue(b + kDepth, inc(kb, kDepth, nbuf));  // block b-1's buffer is free now
+      kb = kp1;
+      xb = inc(xb, NB, g.nx);
     }
     __syncthreads();
     if (threadIdx.x < nbuf) {
