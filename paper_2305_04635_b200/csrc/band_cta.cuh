@@ -266,19 +266,25 @@ struct CtaBand {
   }
 
   // async load of columns [jlo, jhi) (and their rhs entries); complete with wait_cols()
-  __device__ void load_cols(int jlo, int jhi) {
+  // sj: ring slot of column jlo when the caller knows it (saves a division), else -1
+  __device__ void load_cols(int jlo, int jhi, int sj = -1) {
+    if (sj < 0) sj = jlo % g.nslot;
     if (fast) {
       if (threadIdx.x == kCopyThread) {
         bulk_wait_read0();  // the write-back that read these slots is done reading
         const unsigned col = (unsigned)g.ldab * sizeof(double);
         mbar_expect_tx(bars, (unsigned)(jhi - jlo) * col);
-        const int s0 = jlo % g.nslot;
+        const int s0 = sj;
         const int c1 = min(jhi - jlo, g.nslot - s0);
         bulk_g2s(win + (size_t)s0 * g.lds, ab + (int64_t)jlo * g.ldab, c1 * col, bars);
         if (c1 < jhi - jlo) bulk_g2s(win, ab + (int64_t)(jlo + c1) * g.ldab, (jhi - jlo - c1) * col, bars);
       }
       if (kSolve) {
-        for (int j = jlo + threadIdx.x; j < jhi; j += kCtaThreads) cp_async8(bw + (j % g.nslot), rhs + j);
+        for (int j = jlo + threadIdx.x; j < jhi; j += kCtaThreads) {
+          int sl = sj + (j - jlo);
+          if (sl >= g.nslot) sl -= g.nslot;
+          cp_async8(bw + sl, rhs + j);
+        }
         cp_async_commit();
       }
       pending = true;
@@ -322,11 +328,11 @@ struct CtaBand {
 
   // Panel columns [j0, j0+nb) back to HBM (final L).  Call after a barrier that
   // follows fence_async_smem() by every writer; the bulk part is issued by thread 0.
-  __device__ void store_cols(int j0, int nb) {
+  __device__ void store_cols(int j0, int nb, int sj = -1) {  // sj: ring slot of column j0
     if (fast) {
       if (threadIdx.x == kCopyThread) {
         const unsigned col = (unsigned)g.ldab * sizeof(double);
-        const int s0 = j0 % g.nslot;
+        const int s0 = sj >= 0 ? sj : j0 % g.nslot;
         const int c1 = min(nb, g.nslot - s0);
         bulk_s2g(ab + (int64_t)j0 * g.ldab, win + (size_t)s0 * g.lds, c1 * col);
         if (c1 < nb) bulk_s2g(ab + (int64_t)(j0 + c1) * g.ldab, win, (nb - c1) * col);
@@ -653,11 +659,13 @@ struct CtaBand {
       if (pending) wait_cols();  // columns prefetched by the previous step
       else __syncthreads();
       if (threadIdx.x < 32) trace_stamp(step, 1);
-      store_cols(j0, nb);
+      store_cols(j0, nb, kSolve ? s0 : -1);
       // prefetch the columns step k+1 brings into the window (into the slots just
       // written back, once the write-back has read them)
       const int jlo = j0 + NB + kd;
-      if (jlo < n) load_cols(jlo, min(n, jlo + NB));
+      // (the slot hints measured faster in the fused kernel only; the factor-only kernel
+      // keeps the self-computed slots)
+      if (jlo < n) load_cols(jlo, min(n, jlo + NB), kSolve ? slot_from(s0, j0, jlo) : -1);
       if (threadIdx.x < 32) trace_stamp(step, 2);
       if (j0 + nb >= n) break;
       jp = j0; sp = s0; nbp = nb; mp = m;
