@@ -76,6 +76,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// plain (count) arrival, release semantics at CTA scope
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// named barrier over `count` threads (warps of the pipelined factorization)
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 // shared -> global (bulk group)
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
@@ -174,7 +182,8 @@ __host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom&
 
 // Shared-memory footprint (bytes) of one CTA for block size NB.
 __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g, bool solve) {
-  size_t d = (size_t)g.nslot * g.lds + cta_panel_doubles(nb_block, g, solve) + (size_t)nb_block * (nb_block + 4) +
+  // D: two L11 / L11^-1 buffers (the pipelined factorization alternates them by step)
+  size_t d = (size_t)g.nslot * g.lds + cta_panel_doubles(nb_block, g, solve) + 2 * (size_t)nb_block * (nb_block + 4) +
              nb_block + 32;
   if (solve) d += (size_t)g.nx + (size_t)(g.nslot / nb_block) * nb_block;  // rhs ring + staged y
   return d * sizeof(double) + 64;
@@ -195,12 +204,40 @@ struct CtaBand {
   double* bw;                // ring of rhs / solution entries, slot(i) like columns
   double* yb;                // backward sweep: nbuf x NB staged y entries; factor: y of the last two blocks
   unsigned long long* bars;  // mbarriers: [0] window loads, [1 + k] backward buffer k
+  unsigned long long* sig;   // pipelined factorization: [0] panel ready, [1] column 0 updated, [2 + (k&1)] update done
   unsigned* bphase;          // smem: parity of the next wait on bars[1 + k]
   unsigned phase = 0;        // parity of the next wait on bars[0] (uniform register)
   bool pending = false;      // a load_cols is in flight
   bool fast = false;         // every column chunk meets the bulk-copy alignment rules
-  int pw = 0;                // the POTRF warp; warp pw + 4 (same SM sub-partition) idles in the lookahead
+  // Warp roles by SM sub-partition (set_roles): the POTRF warp pw and a light warp share
+  // SMSP 0 with the other CTA's pivot; the six warps on SMSPs 1-3 run every DMMA.
+  int pw = 0;                // the POTRF warp
+  int wk = -1;               // this warp's worker index 0..5 (-1: pivot or light warp)
   unsigned long long* tr = nullptr;  // trace buffer (block 0 only), see bcg_set_trace
+
+  // Roles from the hardware warp slot (%warpid & 3 = SMSP): the second CTA on an SM is
+  // rotated by one sub-partition (tools/micro/warpid.cu), so warp index alone cannot tell.
+  // s_sp: kCtaWarps ints of shared scratch.  Call by all threads, before any role is used.
+  __device__ void set_roles(int* s_sp) {
+    const int warp = threadIdx.x >> 5;
+    unsigned hw;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(hw));
+    if ((threadIdx.x & 31) == 0) s_sp[warp] = (int)(hw & 3);
+    __syncthreads();
+    int n0 = 0, first0 = -1;
+    for (int w = 0; w < kCtaWarps; ++w)
+      if (s_sp[w] == 0) { ++n0; if (first0 < 0) first0 = w; }
+    const bool hwmap = n0 == 2;  // else: fall back to warp index mod 4
+    pw = hwmap ? first0 : 0;
+    int idx = 0, mine = -1;
+    for (int w = 0; w < kCtaWarps; ++w) {
+      if ((hwmap ? s_sp[w] : (w & 3)) == 0) continue;
+      if (w == warp) mine = idx;
+      ++idx;
+    }
+    wk = warp_uniform(mine);
+    __syncthreads();
+  }
 
   __device__ __forceinline__ void trace_stamp(int j, int ph) const {
 #ifdef BCG_TRACE
@@ -468,12 +505,13 @@ struct CtaBand {
   // Panel TRSM as a product: X = A L11^-T for the m panel rows, 16-row tiles over the
   // warps, DMMA m8n8k4 with A from the window (entries outside the band read as 0) and
   // B(k, c) = Linv(c, k) from D.  X goes to the dense panel P and back to the window.
-  __device__ void trsm_panel(int s0, int j0, int nb, int m) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Tiles t = wid, wid + nw, ... (the calling warp is worker wid of nw).
+  __device__ void trsm_panel(int s0, int j0, int nb, int m, int wid, int nw) {
+    const int lane = threadIdx.x & 31;
     const int gr = lane >> 2, gc = lane & 3;
     const int sw = g.nslot - s0;
     const int T = (m + 15) >> 4;
-    for (int t = warp; t < T; t += kCtaWarps) {
+    for (int t = wid; t < T; t += nw) {
       const bool tail = 16 * t + 8 >= m;  // rows 16t+8.. are all past m
       double acc[2][NB / 8][2];
 #pragma unroll
@@ -497,8 +535,8 @@ struct CtaBand {
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int v = 0; v < NB / 8; ++v)
-            if (u == 0 || !tail) dmma884(acc[u][v][0], acc[u][v][1], a[u], bf[v]);
+          for (int v = 0; v < NB / 8; ++v)  // L11^-T is upper triangular: k > 8v+7 adds zeros
+            if ((u == 0 || !tail) && kk <= 2 * v + 1) dmma884(acc[u][v][0], acc[u][v][1], a[u], bf[v]);
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -599,8 +637,205 @@ struct CtaBand {
     }
   }
 
+  // ---- pipelined factorization (kd >= 32) -------------------------------------------
+  // Three warp roles, no CTA-wide barrier inside the column loop:
+  //   pivot (SMSP 0): SYRK of tile (0,0) of update(k-1) -> POTRF(k) (+ L11^-1, + forward
+  //                   sweep) -> TRSM of panel tile 0 -> signal sig[0] ("panel k ready")
+  //   workers (6, SMSPs 1-3): TRSM of panel tiles 1.. -> column 0 of update(k) (signal
+  //                   sig[1]) -> the rest of update(k) (signal sig[2 + (k&1)])
+  //   light (SMSP 0): write-back of panel k, prefetch of the columns update(k+1) needs
+  // The pivot's chain per step is SYRK + POTRF + one 16x16 TRSM; it waits on update(k-2)
+  // (finished a whole step earlier) and on column 0 of update(k-1) (one tile per worker,
+  // done while the pivot runs its POTRF), so it normally never stalls.  Every mbarrier is
+  // at most one phase ahead of its waiters (W is double-buffered by step parity).
+  static constexpr int kWorkers = kCtaWarps - 2;
+  static constexpr int kBarA = 2, kBarB = 3;  // named barriers (1 is the backward sweep's)
+
+  // light warp: panel write-back (lane 0 issues bulk copies; element-wise when not fast)
+  __device__ void light_store(int j0, int nb, int sj) {
+    const int lane = threadIdx.x & 31;
+    if (fast) {
+      if (lane == 0) {
+        const unsigned col = (unsigned)g.ldab * sizeof(double);
+        const int c1 = min(nb, g.nslot - sj);
+        bulk_s2g(ab + (int64_t)j0 * g.ldab, win + (size_t)sj * g.lds, c1 * col);
+        if (c1 < nb) bulk_s2g(ab + (int64_t)(j0 + c1) * g.ldab, win, (nb - c1) * col);
+        bulk_commit();
+      }
+      return;
+    }
+    for (int c = 0; c < nb; ++c) {
+      const int sl = slot_from(sj, j0, j0 + c);
+      for (int o = lane; o < g.ldab; o += 32) ab[(int64_t)(j0 + c) * g.ldab + o] = win[sl * g.lds + o];
+    }
+    __syncwarp();
+  }
+  // light warp: columns [jlo, jhi) (+ their rhs entries) into the ring from slot sj on;
+  // completes one phase of bars[0]
+  __device__ void light_load(int jlo, int jhi, int sj) {
+    const int lane = threadIdx.x & 31;
+    if (fast) {
+      if (lane == 0) {
+        bulk_wait_read0();  // the write-back that read these slots is done reading
+        const unsigned col = (unsigned)g.ldab * sizeof(double);
+        mbar_expect_tx(bars, (unsigned)(jhi - jlo) * col);
+        const int c1 = min(jhi - jlo, g.nslot - sj);
+        bulk_g2s(win + (size_t)sj * g.lds, ab + (int64_t)jlo * g.ldab, c1 * col, bars);
+        if (c1 < jhi - jlo) bulk_g2s(win, ab + (int64_t)(jlo + c1) * g.ldab, (jhi - jlo - c1) * col, bars);
+      }
+    } else {
+      for (int j = jlo; j < jhi; ++j) {
+        const int sl = slot_from(sj, jlo, j);
+        for (int o = lane; o < g.ldab; o += 32) win[sl * g.lds + o] = ab[(int64_t)j * g.ldab + o];
+      }
+    }
+    if (kSolve)
+      for (int j = jlo + lane; j < jhi; j += 32) bw[slot_from(sj, jlo, j)] = rhs[j];
+    __syncwarp();
+    if (!fast && lane == 0) mbar_arrive(bars);  // plain arrival: completes the phase
+  }
+
+  __device__ void pivot_loop(int nblk, volatile int* s_fail) {
+    const int n = g.n, kd = g.kd, lane = threadIdx.x & 31;
+    double* const Dbase = D;
+    int s0 = 0, sp = 0, mp = 0;
+    for (int k = 0; k < nblk; ++k) {
+      const int j0 = k * NB, nb = min(NB, n - j0);
+      const int m = min(kd, n - j0 - nb);
+      trace_stamp(k, 0);
+      if (k >= 2) mbar_wait(sig + 2 + (k & 1), ((k - 2) >> 1) & 1);  // update(k-2) complete
+      trace_stamp(k, 1);
+      if (k >= 1) {
+        // tile (0,0) of update(k-1) (this block) and its rhs rows, from P rows 0..15 = X0(k-1)
+        update_tiles(sp, j0 - NB, NB, mp, 0, 1, 0, 1);
+        if (kSolve) update_rhs(sp, j0 - NB, NB, mp, 0, NB, lane, 32);
+        __syncwarp();
+      }
+      trace_stamp(k, 2);
+      D = Dbase + (k & 1) * NB * kLDD;
+      const int f = potrf_diag(s0, j0, nb);
+      trace_stamp(k, 3);
+      // column 0 of update(k-1) done: A(k+1, k) is final and P rows 0..15 are free.  Also
+      // waited when there is no TRSM (last block, failure): it proves every worker and the
+      // light warp consumed sig[0] phase k-1, so sig[0] never runs two phases ahead
+      if (k >= 1) mbar_wait(sig + 1, (k - 1) & 1);
+      trace_stamp(k, 4);
+      if (f >= 0) {
+        if (lane == 0) *s_fail = j0 + f;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sig);
+        break;
+      }
+      if (m > 0) trsm_panel(s0, j0, nb, m, 0, 1 << 20);
+      fence_async_smem();  // L11 and X0 in the window -> the light warp's bulk write-back
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sig);
+      trace_stamp(k, 5);
+      sp = s0;
+      mp = m;
+      s0 += NB;
+      if (s0 >= g.nslot) s0 -= g.nslot;
+    }
+    D = Dbase;
+  }
+
+  __device__ void worker_loop(int nblk, volatile int* s_fail) {
+    const int n = g.n, kd = g.kd, lane = threadIdx.x & 31;
+    double* const Dbase = D;
+    unsigned lph = phase;  // parity of the next window-load completion
+    int s0 = 0;
+    for (int k = 0; k < nblk; ++k) {
+      const int j0 = k * NB, nb = min(NB, n - j0);
+      const int m = min(kd, n - j0 - nb);
+      mbar_wait(sig, k & 1);  // panel k: L11^-1(k) in D, X0 in P rows 0..15
+      if (*s_fail >= 0) break;
+      if (wk == 0) trace_stamp(k, 6);
+      if (k >= 1 && k * NB + kd < n) {  // the columns update(k) brings in (prefetched at k-1)
+        mbar_wait(bars, lph);
+        lph ^= 1u;
+      }
+      named_bar(kBarA, 32 * kWorkers);  // update(k-1) done by every worker
+      D = Dbase + (k & 1) * NB * kLDD;
+      if (m > NB) trsm_panel(s0, j0, nb, m, 1 + wk, kWorkers);
+      fence_async_smem();
+      named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete (+ the light warp)
+      const int T = (m + 15) >> 4;
+      if (kSolve && m > NB) update_rhs(s0, j0, nb, m, NB, 1 << 20, lane + 32 * wk, 32 * kWorkers);
+      update_tiles(s0, j0, nb, m, 1, T, wk, kWorkers);  // tile column 0 (the next panel)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sig + 1);
+      // the rest, starting with the workers that had no column-0 tile
+      const int first = (T - 1) % kWorkers;
+      update_tiles(s0, j0, nb, m, T, 1 << 20, (wk + kWorkers - first) % kWorkers, kWorkers);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sig + 2 + (k & 1));
+      if (wk == 0) trace_stamp(k, 7);
+      s0 += NB;
+      if (s0 >= g.nslot) s0 -= g.nslot;
+    }
+    D = Dbase;
+  }
+
+  __device__ int light_loop(int nblk, volatile int* s_fail) {
+    const int n = g.n, kd = g.kd;
+    int s0 = 0, nload = 0;
+    for (int k = 0; k < nblk; ++k) {
+      const int j0 = k * NB, nb = min(NB, n - j0);
+      mbar_wait(sig, k & 1);
+      if (*s_fail >= 0) break;
+      named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete
+      light_store(j0, nb, s0);
+      const int jlo = j0 + NB + kd;
+      if (jlo < n) {
+        light_load(jlo, min(n, jlo + NB), slot_from(s0, j0, jlo));
+        ++nload;
+      }
+      s0 += NB;
+      if (s0 >= g.nslot) s0 -= g.nslot;
+    }
+    return nload;
+  }
+
+  __device__ int factor_la() {
+    const int n = g.n, kd = g.kd;
+    __shared__ int s_fail, s_nload;
+    const int warp = warp_uniform(threadIdx.x >> 5);
+    init_fast();
+    for (int idx = threadIdx.x; idx < NB * g.pld; idx += kCtaThreads) P[idx] = 0.0;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 4; ++i) mbar_init(sig + i, i == 0 ? 1 : kWorkers);
+      s_fail = -1;
+      s_nload = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    load_cols(0, min(n, kd + NB));
+    wait_cols();  // (CTA barrier: also publishes the mbarrier init)
+    const int nblk = (n + NB - 1) / NB;
+    if (warp == pw) {
+      pivot_loop(nblk, &s_fail);
+    } else if (wk >= 0) {
+      worker_loop(nblk, &s_fail);
+    } else {
+      const int nload = light_loop(nblk, &s_fail);
+      if ((threadIdx.x & 31) == 0) {
+        s_nload = nload;
+        if (nload > 0) mbar_wait(bars, phase ^ ((unsigned)(nload - 1) & 1u));  // the last prefetch landed
+        bulk_wait0();  // write-backs complete
+        fence_async_global();
+      }
+    }
+    __syncthreads();
+    phase ^= (unsigned)s_nload & 1u;
+    const int fail = s_fail;
+    if (threadIdx.x == 0)
+      for (int i = 0; i < 4; ++i) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(sig + i)) : "memory");
+    __syncthreads();
+    return fail < 0 ? -1 : fail;
+  }
+
   // Whole factorization (+ forward sweep when kSolve).  Returns -1 or failing column.
   __device__ int factor() {
+    if (g.kd >= 32) return factor_la();
     const int n = g.n, kd = g.kd;
     __shared__ int s_fail;
     const int warp = threadIdx.x >> 5;
@@ -637,12 +872,11 @@ struct CtaBand {
         const int f = potrf_diag(s0, j0, nb);
         if ((threadIdx.x & 31) == 0) s_fail = f;
         trace_stamp(step, 4);
-      } else if ((wu & 3) != pw && jp >= 0) {
+      } else if (wk >= 0 && jp >= 0) {
         // the rest of the previous step's update, on the other three SM sub-partitions
-        const int wid = wu - (wu > pw) - (wu > pw + 4);
-        update_tiles(sp, jp, nbp, mp, 1, 1 << 20, wid, kCtaWarps - 2);
-        if (kSolve) update_rhs(sp, jp, nbp, mp, NB, 1 << 20, threadIdx.x - 32 * wu + 32 * wid, 32 * (kCtaWarps - 2));
-        if (wu == (pw + 1) % 4) trace_stamp(step, 5);
+        update_tiles(sp, jp, nbp, mp, 1, 1 << 20, wk, kCtaWarps - 2);
+        if (kSolve) update_rhs(sp, jp, nbp, mp, NB, 1 << 20, (threadIdx.x & 31) + 32 * wk, 32 * (kCtaWarps - 2));
+        if (wk == 0) trace_stamp(step, 5);
       }
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(step, 6);
@@ -653,7 +887,10 @@ struct CtaBand {
       }
       const int m = min(kd, n - j0 - nb);
       if (threadIdx.x < 32) trace_stamp(step, 0);
-      trsm_panel(s0, j0, nb, m);
+      // TRSM on the six warps off the POTRF warps' sub-partition: a DMMA queued on that
+      // SMSP stalls the other CTA's pivot chain for hundreds of cycles
+      // (tools/micro/pipe_mix.cu: a dependent DFMA 8.7 -> 73 cycles with one DMMA warp there)
+      if (wk >= 0) trsm_panel(s0, j0, nb, m, wk, kCtaWarps - 2);
       if (threadIdx.x < 32) trace_stamp(step, 7);
       fence_async_smem();  // panel writes -> visible to the bulk write-back
       if (pending) wait_cols();  // columns prefetched by the previous step

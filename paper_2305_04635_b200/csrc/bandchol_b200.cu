@@ -26,6 +26,8 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, i
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) unsigned long long bars[1 + 16];
   __shared__ unsigned bphase[16];
+  __shared__ int s_sp[kCtaWarps];
+  __shared__ __align__(8) unsigned long long sig[4];
   if (threadIdx.x < 17) mbar_init(&bars[threadIdx.x], 1);
   if (threadIdx.x < 16) bphase[threadIdx.x] = 0;
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -36,16 +38,17 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, i
     w.bars = bars;
     w.bphase = bphase;
     w.phase = phase;
-    w.pw = ((blockIdx.x / 148) & 1) ? 2 : 0;
+    w.set_roles(s_sp);
     w.tr = (blockIdx.x == 0 && mat == 0) ? g_trace : nullptr;
     w.ab = ab0 + (int64_t)mat * stride_ab;
     w.rhs = kSolve ? b0 + (int64_t)mat * stride_b : nullptr;
     double* p = smem;
     w.win = p; p += (size_t)g.nslot * g.lds;
     w.P = p; p += cta_panel_doubles(NB, g, kSolve);
-    w.D = p; p += NB * (NB + 4);
+    w.D = p; p += 2 * NB * (NB + 4);
     w.Dinv = p; p += NB;
     w.lbuf = p; p += 32;
+    w.sig = sig;
     w.bw = kSolve ? p : nullptr;
     if (kSolve) p += g.nslot;
     w.yb = kSolve ? p : nullptr;
@@ -86,7 +89,7 @@ pbtrs_cta_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t strid
   double* p = smem;
   w.win = p; p += (size_t)g.nslot * g.lds;
   w.P = p; p += cta_panel_doubles(NB, g, true);
-  w.D = p; p += NB * (NB + 4);
+  w.D = p; p += 2 * NB * (NB + 4);
   w.Dinv = p; p += NB;
   w.lbuf = p; p += 32;
   w.bw = p; p += g.nx;
@@ -179,7 +182,9 @@ bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb, bool solve) {
   if (ns & 1) ++ns;
   g.nslot = ns;
   g.nx = ns;
-  int pld = ((kd + 15) / 16) * 16 + 4;  // covers the 16-row tiles, = 4 (mod 16)
+  // >= kd rows, = 4 (mod 16): conflict-free DMMA fragment loads.  The tile GEMM reads (and
+  // discards) up to 12 rows past kd, i.e. into the next column or the buffer after P.
+  int pld = kd + ((4 - kd % 16) + 16) % 16;
   g.pld = pld;
   return g;
 }

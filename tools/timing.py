@@ -238,3 +238,42 @@ def trace_solve(batch=1):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_solve":
     trace_solve(1)
     trace_solve(296)
+
+
+def trace_la(tag, batch=1):
+    """Phase breakdown of the pipelined one-CTA factorization (block 0, matrix 0).
+
+    Pivot stamps per step: 0 start, 1 after waiting update(k-2), 2 after SYRK(0,0),
+    3 after POTRF, 4 after waiting column 0 of update(k-1), 5 after TRSM + signal;
+    worker 0: 6 after the panel signal, 7 after its share of update(k)."""
+    from paper_2305_04635_b200 import _lib
+    cfg = CONFIGS[tag]
+    n, k = cfg.dim, cfg.bandwidth
+    a = np.stack([generate_spd(n, k, s).data for s in range(min(batch, 8))])
+    a = np.concatenate([a] * ((batch + 7) // 8))[:batch]
+    a0 = torch.from_numpy(a).cuda()
+    buf = torch.zeros(1 + 8 * (n // 16 + 2), dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    w = a0.clone()
+    bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
+    torch.cuda.synchronize()
+    lib.bcg_set_trace(buf.data_ptr(), buf.numel() * 8)
+    w = a0.clone()
+    bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
+    torch.cuda.synchronize()
+    lib.bcg_set_trace(None, 0)
+    t = buf.cpu().numpy()
+    steps = int(t[0])
+    st = t[1:1 + 8 * steps].reshape(steps, 8).astype(np.float64)[2:-2]
+    med = lambda a, b: float(np.median(st[:, b] - st[:, a]))  # noqa: E731  (SM cycles)
+    out = {"config": tag, "batch": batch, "steps": steps, "unit": "cycles",
+           "wait_W": med(0, 1), "syrk": med(1, 2), "potrf": med(2, 3), "wait_W1": med(3, 4),
+           "trsm_signal": med(4, 5), "worker_wake": med(5, 6), "worker_step": med(6, 7),
+           "step": float(np.median(np.diff(st[:, 0])))}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_la":
+    trace_la("C1", 1)
+    trace_la("C5", 1)
+    trace_la("C5", 296)
