@@ -134,6 +134,12 @@ __device__ __forceinline__ double shfl_early(double v, int src) {
   return r;
 }
 
+// d -= a b (negated A operand; not volatile, so the scheduler may interleave chains)
+__device__ __forceinline__ void dmma884n(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(-a), "d"(b));
+}
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -560,9 +566,64 @@ struct CtaBand {
   // Tiles are numbered column by column ((0,0), (1,0), ..., (T-1,0), (1,1), ...); the
   // calling warp (rank wid of nw workers) takes tiles first + wid, first + wid + nw, ...
   // below `last`.
-  __device__ void update_tiles(int s0, int j0, int nb, int m, int first, int last, int wid, int nw) {
+  // One 16x16 tile C(i0.., q0..) -= P(i0..) P(q0..)^T.  DIAG: a diagonal tile (the 8x8
+  // block above the diagonal is skipped, the two diagonal 8x8 blocks are masked to q <= i);
+  // ROWS: 0 every row < m, 1 rows i0+8.. partly past m (masked), 2 rows i0+8.. all past m
+  // (their two 8x8 blocks skipped).  Straight-line per kind, so every accumulator chain
+  // of the tile is in flight at once.
+  template <bool DIAG, int ROWS>
+  __device__ __forceinline__ void tile_update(const int (&cb)[2][2], int i0, int q0, int m) {
     const int lane = threadIdx.x & 31;
     const int gr = lane >> 2, gc = lane & 3;
+    constexpr bool kU1 = ROWS != 2;   // rows i0+8.. computed
+    constexpr bool kV1 = !DIAG;       // block (0,1) computed
+    auto ok = [&](int u, int v, int e) {
+      const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
+      bool r = true;
+      if (DIAG && u == v) r = q <= i;
+      if (ROWS != 0 && (u == 1 || ROWS == 2)) r = r && i < m;
+      return r;
+    };
+    double acc[2][2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if ((u == 1 && !kU1) || (u == 0 && v == 1 && !kV1)) { acc[u][v][e] = 0.0; continue; }
+          const int i = i0 + u * 8 + gr;
+          acc[u][v][e] = ok(u, v, e) ? win[cb[v][e] + i] : 0.0;
+        }
+#pragma unroll
+    for (int k0 = 0; k0 < NB; k0 += 4) {
+      const double* pk = P + (k0 + gc) * g.pld;
+      const double a0 = pk[i0 + gr], a1 = kU1 ? pk[i0 + 8 + gr] : 0.0;
+      const double b0 = pk[q0 + gr], b1 = pk[q0 + 8 + gr];
+      dmma884n(acc[0][0][0], acc[0][0][1], a0, b0);
+      if (kU1) dmma884n(acc[1][0][0], acc[1][0][1], a1, b0);
+      if (kV1) dmma884n(acc[0][1][0], acc[0][1][1], a0, b1);
+      if (kU1) dmma884n(acc[1][1][0], acc[1][1][1], a1, b1);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if ((u == 1 && !kU1) || (u == 0 && v == 1 && !kV1)) continue;
+          const int i = i0 + u * 8 + gr;
+          if (ok(u, v, e)) win[cb[v][e] + i] = acc[u][v][e];
+        }
+  }
+
+  // Trailing update of 16x16 tiles, C(i,j) -= sum_c P(i,c) P(j,c), i,j < m, lower only.
+  // Tiles are numbered column by column ((0,0), (1,0), ..., (T-1,0), (1,1), ...); the
+  // calling warp (rank wid of nw workers) takes tiles first + wid, first + wid + nw, ...
+  // below `last`.
+  __device__ void update_tiles(int s0, int j0, int nb, int m, int first, int last, int wid, int nw) {
+    const int lane = threadIdx.x & 31;
+    const int gc = lane & 3;
     const int base = j0 + nb;
     const int T = (m + 15) >> 4;
     int tj = 0, ti = first + wid, left = last - first - wid;
@@ -578,45 +639,16 @@ struct CtaBand {
           const int q = q0 + v * 8 + 2 * gc + e;
           cb[v][e] = slot_from(s0, j0, base + (q < m ? q : 0)) * g.lds - q;
         }
-      double acc[2][2][2];
-      // interior tile (below the diagonal, every row < m): no masks
-      const bool full = ti > tj && i0 + 16 <= m;
-      const bool diag = ti == tj, tail = i0 + 8 >= m;
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int v = 0; v < 2; ++v)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
-            const bool ok = full || ((i < m) && (q <= i));
-            acc[u][v][e] = ok ? win[cb[v][e] + i] : 0.0;
-          }
-#pragma unroll
-      for (int k0 = 0; k0 < NB; k0 += 4) {
-        const double* pk = P + (k0 + gc) * g.pld;
-        double a[2], b[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) a[u] = -pk[i0 + u * 8 + gr];
-#pragma unroll
-        for (int v = 0; v < 2; ++v) b[v] = pk[q0 + v * 8 + gr];
-        // skip the 8x8 blocks that are all padding rows (past m) or all above the diagonal
-        dmma884(acc[0][0][0], acc[0][0][1], a[0], b[0]);
-        if (!diag) dmma884(acc[0][1][0], acc[0][1][1], a[0], b[1]);
-        if (!tail) {
-          dmma884(acc[1][0][0], acc[1][0][1], a[1], b[0]);
-          dmma884(acc[1][1][0], acc[1][1][1], a[1], b[1]);
-        }
+      const int rows = i0 + 16 <= m ? 0 : (i0 + 8 < m ? 1 : 2);
+      if (ti != tj) {
+        if (rows == 0) tile_update<false, 0>(cb, i0, q0, m);
+        else if (rows == 1) tile_update<false, 1>(cb, i0, q0, m);
+        else tile_update<false, 2>(cb, i0, q0, m);
+      } else {
+        if (rows == 0) tile_update<true, 0>(cb, i0, q0, m);
+        else if (rows == 1) tile_update<true, 1>(cb, i0, q0, m);
+        else tile_update<true, 2>(cb, i0, q0, m);
       }
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int v = 0; v < 2; ++v)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
-            if (full || ((i < m) && (q <= i))) win[cb[v][e] + i] = acc[u][v][e];
-          }
       ti += nw;
       left -= nw;
       while (tj < T && ti >= T) { ti += tj + 1 - T; ++tj; }
@@ -749,27 +781,33 @@ struct CtaBand {
       const int m = min(kd, n - j0 - nb);
       mbar_wait(sig, k & 1);  // panel k: L11^-1(k) in D, X0 in P rows 0..15
       if (*s_fail >= 0) break;
-      if (wk == 0) trace_stamp(k, 6);
+      const int tw = nblk + 1 + k;  // worker 0's trace row
+      if (wk == 0) { trace_stamp(k, 6); trace_stamp(tw, 0); }
       if (k >= 1 && k * NB + kd < n) {  // the columns update(k) brings in (prefetched at k-1)
         mbar_wait(bars, lph);
         lph ^= 1u;
       }
+      if (wk == 0) trace_stamp(tw, 1);
       named_bar(kBarA, 32 * kWorkers);  // update(k-1) done by every worker
+      if (wk == 0) trace_stamp(tw, 2);
       D = Dbase + (k & 1) * NB * kLDD;
       if (m > NB) trsm_panel(s0, j0, nb, m, 1 + wk, kWorkers);
       fence_async_smem();
+      if (wk == 0) trace_stamp(tw, 3);
       named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete (+ the light warp)
+      if (wk == 0) trace_stamp(tw, 4);
       const int T = (m + 15) >> 4;
       if (kSolve && m > NB) update_rhs(s0, j0, nb, m, NB, 1 << 20, lane + 32 * wk, 32 * kWorkers);
       update_tiles(s0, j0, nb, m, 1, T, wk, kWorkers);  // tile column 0 (the next panel)
       __syncwarp();
       if (lane == 0) mbar_arrive(sig + 1);
+      if (wk == 0) trace_stamp(tw, 5);
       // the rest, starting with the workers that had no column-0 tile
       const int first = (T - 1) % kWorkers;
       update_tiles(s0, j0, nb, m, T, 1 << 20, (wk + kWorkers - first) % kWorkers, kWorkers);
       __syncwarp();
       if (lane == 0) mbar_arrive(sig + 2 + (k & 1));
-      if (wk == 0) trace_stamp(k, 7);
+      if (wk == 0) { trace_stamp(k, 7); trace_stamp(tw, 6); }
       s0 += NB;
       if (s0 >= g.nslot) s0 -= g.nslot;
     }

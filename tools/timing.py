@@ -252,7 +252,8 @@ def trace_la(tag, batch=1):
     a = np.stack([generate_spd(n, k, s).data for s in range(min(batch, 8))])
     a = np.concatenate([a] * ((batch + 7) // 8))[:batch]
     a0 = torch.from_numpy(a).cuda()
-    buf = torch.zeros(1 + 8 * (n // 16 + 2), dtype=torch.int64, device="cuda")
+    nblk = (n + 15) // 16
+    buf = torch.zeros(1 + 8 * (2 * nblk + 4), dtype=torch.int64, device="cuda")
     lib = _lib.load()
     w = a0.clone()
     bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
@@ -263,13 +264,18 @@ def trace_la(tag, batch=1):
     torch.cuda.synchronize()
     lib.bcg_set_trace(None, 0)
     t = buf.cpu().numpy()
-    steps = int(t[0])
-    st = t[1:1 + 8 * steps].reshape(steps, 8).astype(np.float64)[2:-2]
+    steps = nblk
+    allst = t[1:].reshape(-1, 8).astype(np.float64)
+    st = allst[:nblk][2:-2]
+    wt = allst[nblk + 1: 2 * nblk + 1][2:-2]
+    wmed = lambda a, b: float(np.median(wt[:, b] - wt[:, a]))  # noqa: E731
     med = lambda a, b: float(np.median(st[:, b] - st[:, a]))  # noqa: E731  (SM cycles)
     out = {"config": tag, "batch": batch, "steps": steps, "unit": "cycles",
            "wait_W": med(0, 1), "syrk": med(1, 2), "potrf": med(2, 3), "wait_W1": med(3, 4),
            "trsm_signal": med(4, 5), "worker_wake": med(5, 6), "worker_step": med(6, 7),
-           "step": float(np.median(np.diff(st[:, 0])))}
+           "step": float(np.median(np.diff(st[:, 0]))),
+           "w_load": wmed(0, 1), "w_barA": wmed(1, 2), "w_trsm": wmed(2, 3), "w_barB": wmed(3, 4),
+           "w_col0": wmed(4, 5), "w_rest": wmed(5, 6)}
     print(json.dumps(out), flush=True)
 
 
