@@ -186,12 +186,18 @@ __host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom&
   return (solve && inv > p) ? inv : p;
 }
 
+// Column-block buffers of the streamed sweeps: kDepth (4) blocks in flight + the current.
+__host__ __device__ inline int cta_sweep_buffers(int nb_block, const CtaGeom& g) {
+  const int n = g.nslot / nb_block;
+  return n < 5 ? n : 5;
+}
+
 // Shared-memory footprint (bytes) of one CTA for block size NB.
 __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g, bool solve) {
   // D: two L11 / L11^-1 buffers (the pipelined factorization alternates them by step)
   size_t d = (size_t)g.nslot * g.lds + cta_panel_doubles(nb_block, g, solve) + 2 * (size_t)nb_block * (nb_block + 4) +
-             nb_block + 32;
-  if (solve) d += (size_t)g.nx + (size_t)(g.nslot / nb_block) * nb_block;  // rhs ring + staged y
+             nb_block;
+  if (solve) d += (size_t)g.nx + (size_t)cta_sweep_buffers(nb_block, g) * nb_block;  // rhs ring + staged y
   return d * sizeof(double) + 64;
 }
 
@@ -205,8 +211,9 @@ struct CtaBand {
   double* P;                 // NB x pld dense panel, P[c*pld + r] = L(j0+nb+r, j0+c)
   static constexpr int kLDD = NB + 4;  // D stride (= 4 mod 16: conflict-free DMMA fragments)
   double* D;                 // L11, D[c*kLDD + r] = L(r, c); then L11^-1, D[i*kLDD + j] = Linv(i, j)
-  double* Dinv;              // NB doubles of scratch (+ lbuf: the backward sweep's far sums)
-  double* lbuf;              // 32 doubles: sink for the inverse lanes' column stores
+  double* Dinv;              // 3 x NB doubles of sweep scratch (aliases the second D buffer,
+                             // free outside the factorization)
+  double* lbuf;              // NB doubles: sink for the inverse lanes' column stores
   double* bw;                // ring of rhs / solution entries, slot(i) like columns
   double* yb;                // backward sweep: nbuf x NB staged y entries; factor: y of the last two blocks
   unsigned long long* bars;  // mbarriers: [0] window loads, [1 + k] backward buffer k
@@ -406,6 +413,7 @@ struct CtaBand {
   // column suffices), lanes NB..31 build L11^-1 along the way, and failure is found
   // once at the end: after a non-positive / NaN pivot every later pivot of the block is
   // NaN, so the first failing column is the first lane whose L(r, r) is not > 0.
+  template <bool kFwd>
   __device__ int potrf_diag(int s0, int j0, int nb) {
     const int r = threadIdx.x & 31;
     double row[NB];
@@ -434,7 +442,7 @@ struct CtaBand {
       }
     }
     double s = 0.0;
-    if (kSolve && r < nb) s = bw[slot_from(s0, j0, j0 + r)];
+    if (kFwd && r < nb) s = bw[slot_from(s0, j0, j0 + r)];
     // chain state, identical in every lane: p = pivot of column c, (alpha, beta) =
     // (A'(c+1,c), A'(c+1,c+1)) through column c-1, broadcast by lane c+1 a step early.
     double p = __shfl_sync(kFull, row[0], 0);
@@ -461,7 +469,7 @@ struct CtaBand {
         alpha_n = shfl_early(row[c + 1 < NB ? c + 1 : 0], c + 2);
         beta_n = shfl_early(bn, c + 2);
       }
-      if (kSolve) {
+      if (kFwd) {
         const double yc = __shfl_sync(kFull, s, c) * rs;
         s = (r == c) ? yc : ((r > c) ? fma(-lrc, yc, s) : s);
       }
@@ -493,7 +501,7 @@ struct CtaBand {
       const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
       if (c <= r && r < nb && r - c <= g.kd) win[sl * g.lds + (r - c)] = row[c];
     }
-    if (kSolve && r < nb) {
+    if (kFwd && r < nb) {
       bw[slot_from(s0, j0, j0 + r)] = s;
       rhs[j0 + r] = s;
       yb[((j0 / NB) & 1) * NB + r] = s;  // y of this block for update_rhs (ring slot is reused)
@@ -512,7 +520,9 @@ struct CtaBand {
   // warps, DMMA m8n8k4 with A from the window (entries outside the band read as 0) and
   // B(k, c) = Linv(c, k) from D.  X goes to the dense panel P and back to the window.
   // Tiles t = wid, wid + nw, ... (the calling warp is worker wid of nw).
-  __device__ void trsm_panel(int s0, int j0, int nb, int m, int wid, int nw) {
+  // rhs: also b(rows of the tile) -= X y (y = this step's forward-sweep block in yb) as
+  // DMMA with y in column 0 of B, so no scalar FP64 chain runs on a DMMA-busy SMSP.
+  __device__ void trsm_panel(int s0, int j0, int nb, int m, int wid, int nw, bool rhs = false) {
     const int lane = threadIdx.x & 31;
     const int gr = lane >> 2, gc = lane & 3;
     const int sw = g.nslot - s0;
@@ -558,6 +568,30 @@ struct CtaBand {
             P[c * g.pld + r] = acc[u][v][e];
             if (c < nb && off <= g.kd) win[sl * g.lds + off] = acc[u][v][e];
           }
+      }
+      if (kSolve && rhs) {
+        __syncwarp();  // X of this tile in P (A operand); B(kk, n) = y_kk for n == 0
+        const double* y = yb + ((j0 / NB) & 1) * NB;
+        double cr[2][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int r = 16 * t + 8 * u + gr;
+          cr[u][0] = (gc == 0 && r < m) ? bw[slot_from(s0, j0, j0 + nb + r)] : 0.0;
+          cr[u][1] = 0.0;
+        }
+#pragma unroll
+        for (int kk = 0; kk < NB / 4; ++kk) {
+          const int k = 4 * kk + gc;
+          const double bfr = (gr == 0 && k < nb) ? y[k] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (u == 0 || !tail) dmma884n(cr[u][0], cr[u][1], P[k * g.pld + 16 * t + 8 * u + gr], bfr);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int r = 16 * t + 8 * u + gr;
+          if (gc == 0 && r < m) bw[slot_from(s0, j0, j0 + nb + r)] = cr[u][0];
+        }
       }
     }
   }
@@ -721,10 +755,53 @@ struct CtaBand {
         for (int o = lane; o < g.ldab; o += 32) win[sl * g.lds + o] = ab[(int64_t)j * g.ldab + o];
       }
     }
-    if (kSolve)
-      for (int j = jlo + lane; j < jhi; j += 32) bw[slot_from(sj, jlo, j)] = rhs[j];
+    if (kSolve) {  // rhs entries: cp.async, completed before the next barrier B (light_loop)
+      for (int j = jlo + lane; j < jhi; j += 32) cp_async8(bw + slot_from(sj, jlo, j), rhs + j);
+      cp_async_commit();
+    }
     __syncwarp();
     if (!fast && lane == 0) mbar_arrive(bars);  // plain arrival: completes the phase
+  }
+
+  // Fused solve, pivot warp: y_k = L11^-1 s_k once L11^-1 is in D (a 16 x 16 product: two
+  // half rows per lane, 4-deep chains; the substitution inside the POTRF loop would add a
+  // shuffle chain to every column), to rhs (global, for the backward sweep) and yb.
+  __device__ void forward_block(int k, int j0, int nb, int s0) {
+    const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
+    const double* li = D + r * kLDD + 8 * h;  // Linv(r, 8h..), row-major
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      const int j = 8 * h + t;
+      const double s0v = j < nb ? bw[slot_from(s0, j0, j0 + j)] : 0.0;
+      const double s1v = j + 1 < nb ? bw[slot_from(s0, j0, j0 + j + 1)] : 0.0;
+      a0 = fma(li[t], s0v, a0);
+      a1 = fma(li[t + 1], s1v, a1);
+    }
+    double y = a0 + a1;
+    y += __shfl_down_sync(kFull, y, 16);
+    if (lane < nb) {
+      rhs[j0 + lane] = y;
+      yb[(k & 1) * NB + lane] = y;
+    }
+    __syncwarp();
+  }
+
+  // Fused solve, pivot warp: block k+1's rhs rows lose X0(k) y_k (X0 in P rows 0..15, y_k in
+  // yb).  Lane (r, h) sums half h of row r's products; the halves meet by shuffle.
+  __device__ void rhs_next_block(int k, int j0, int nb, int m, int s0) {
+    const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
+    const double* y = yb + (k & 1) * NB + 8 * h;
+    double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      b0 = fma(P[(8 * h + t) * g.pld + r], y[t], b0);
+      b1 = fma(P[(8 * h + t + 1) * g.pld + r], y[t + 1], b1);
+    }
+    double u = b0 + b1;
+    u += __shfl_down_sync(kFull, u, 16);
+    if (lane < min(NB, m)) bw[slot_from(s0, j0, j0 + nb + lane)] -= u;
+    __syncwarp();
   }
 
   __device__ void pivot_loop(int nblk, volatile int* s_fail) {
@@ -740,12 +817,12 @@ struct CtaBand {
       if (k >= 1) {
         // tile (0,0) of update(k-1) (this block) and its rhs rows, from P rows 0..15 = X0(k-1)
         update_tiles(sp, j0 - NB, NB, mp, 0, 1, 0, 1);
-        if (kSolve) update_rhs(sp, j0 - NB, NB, mp, 0, NB, lane, 32);
         __syncwarp();
       }
       trace_stamp(k, 2);
       D = Dbase + (k & 1) * NB * kLDD;
-      const int f = potrf_diag(s0, j0, nb);
+      const int f = potrf_diag<false>(s0, j0, nb);
+      if (kSolve && f < 0) forward_block(k, j0, nb, s0);
       trace_stamp(k, 3);
       // column 0 of update(k-1) done: A(k+1, k) is final and P rows 0..15 are free.  Also
       // waited when there is no TRSM (last block, failure): it proves every worker and the
@@ -762,6 +839,9 @@ struct CtaBand {
       fence_async_smem();  // L11 and X0 in the window -> the light warp's bulk write-back
       __syncwarp();
       if (lane == 0) mbar_arrive(sig);
+      // block k+1's rhs rows (read by POTRF(k+1)); P rows 0..15 stay X0(k) until this
+      // warp's next TRSM
+      if (kSolve && m > 0) rhs_next_block(k, j0, nb, m, s0);
       trace_stamp(k, 5);
       sp = s0;
       mp = m;
@@ -781,7 +861,7 @@ struct CtaBand {
       const int m = min(kd, n - j0 - nb);
       mbar_wait(sig, k & 1);  // panel k: L11^-1(k) in D, X0 in P rows 0..15
       if (*s_fail >= 0) break;
-      const int tw = nblk + 1 + k;  // worker 0's trace row
+      const int tw = 2 * nblk + 2 + k;  // worker 0's trace row (after the backward sweep's)
       if (wk == 0) { trace_stamp(k, 6); trace_stamp(tw, 0); }
       if (k >= 1 && k * NB + kd < n) {  // the columns update(k) brings in (prefetched at k-1)
         mbar_wait(bars, lph);
@@ -791,16 +871,17 @@ struct CtaBand {
       named_bar(kBarA, 32 * kWorkers);  // update(k-1) done by every worker
       if (wk == 0) trace_stamp(tw, 2);
       D = Dbase + (k & 1) * NB * kLDD;
-      if (m > NB) trsm_panel(s0, j0, nb, m, 1 + wk, kWorkers);
+      // (fused solve: each TRSM tile also takes X y_k off its rhs rows, on the tensor path)
+      if (m > NB) trsm_panel(s0, j0, nb, m, 1 + wk, kWorkers, kSolve);
       fence_async_smem();
       if (wk == 0) trace_stamp(tw, 3);
       named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete (+ the light warp)
       if (wk == 0) trace_stamp(tw, 4);
       const int T = (m + 15) >> 4;
-      if (kSolve && m > NB) update_rhs(s0, j0, nb, m, NB, 1 << 20, lane + 32 * wk, 32 * kWorkers);
       update_tiles(s0, j0, nb, m, 1, T, wk, kWorkers);  // tile column 0 (the next panel)
       __syncwarp();
       if (lane == 0) mbar_arrive(sig + 1);
+      // forward sweep: rows of panel tiles 1.. lose X y_k
       if (wk == 0) trace_stamp(tw, 5);
       // the rest, starting with the workers that had no column-0 tile
       const int first = (T - 1) % kWorkers;
@@ -821,6 +902,7 @@ struct CtaBand {
       const int j0 = k * NB, nb = min(NB, n - j0);
       mbar_wait(sig, k & 1);
       if (*s_fail >= 0) break;
+      if (kSolve) cp_async_wait_all();  // rhs entries of the rows the previous prefetch brought in
       named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete
       light_store(j0, nb, s0);
       const int jlo = j0 + NB + kd;
@@ -855,6 +937,7 @@ struct CtaBand {
       worker_loop(nblk, &s_fail);
     } else {
       const int nload = light_loop(nblk, &s_fail);
+      if (kSolve) cp_async_wait_all();
       if ((threadIdx.x & 31) == 0) {
         s_nload = nload;
         if (nload > 0) mbar_wait(bars, phase ^ ((unsigned)(nload - 1) & 1u));  // the last prefetch landed
@@ -907,7 +990,7 @@ struct CtaBand {
           __syncwarp();
         }
         trace_stamp(step, 3);
-        const int f = potrf_diag(s0, j0, nb);
+        const int f = potrf_diag<kSolve>(s0, j0, nb);
         if ((threadIdx.x & 31) == 0) s_fail = f;
         trace_stamp(step, 4);
       } else if (wk >= 0 && jp >= 0) {
@@ -1015,9 +1098,9 @@ struct CtaBand {
     const int n = g.n, kd = g.kd;
     const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
     constexpr int kDepth = 4;
-    const int nbuf = g.nslot / NB;
+    const int nbuf = cta_sweep_buffers(NB, g);
     const int nblk = (n + NB - 1) / NB;
-    double* ycur = Dinv;  // y of the last two blocks (Dinv + lbuf: 2 x NB)
+    double* ycur = Dinv;  // y of the last two blocks (2 x NB)
     double* li_buf = P;
     // parity of the next wait on buffer k (bit k) and ring positions, tracked without divisions
     unsigned pbits = 0;
@@ -1092,7 +1175,7 @@ struct CtaBand {
           }
           v -= a0 + a1;
         }
-        double* ss = lbuf + NB;  // (ycur = Dinv + lbuf[0, NB))
+        double* ss = Dinv + 2 * NB;
         if (r < NB) ss[r] = v;
         __syncwarp();
         const double* li = li_buf + (b & 1) * NB * kLDD + (r < NB ? r : 0) * kLDD;
@@ -1178,7 +1261,7 @@ struct CtaBand {
     const int n = g.n;
     const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
     constexpr int kDepth = 4;
-    const int nbuf = g.nslot / NB;  // >= kDepth + 1 (host guarantees nslot >= (kDepth+1)*NB)
+    const int nbuf = cta_sweep_buffers(NB, g);  // >= kDepth + 1 (host guarantees nslot >= (kDepth+1)*NB)
     const int nblk = (n + NB - 1) / NB;
     double* sfar = Dinv;            // 2 x NB: far part (incl. y) per block, double-buffered
     const bool bulk_y = fast && !(((uintptr_t)rhs) & 15);
@@ -1312,7 +1395,7 @@ struct CtaBand {
           v -= a0 + a1;
         }
         // x_b = L11^-T s_b: lane r dots column r of L11^-1 with s (no sequential chain)
-        double* ss = lbuf + NB;  // (lbuf[0, NB) is the second half of sfar)
+        double* ss = Dinv + 2 * NB;
         if (r < NB) ss[r] = v;
         __syncwarp();
         const double* li = li_buf + (b & 1) * NB * kLDD + (r < NB ? r : 0) * kLDD;

@@ -46,8 +46,8 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, i
     w.win = p; p += (size_t)g.nslot * g.lds;
     w.P = p; p += cta_panel_doubles(NB, g, kSolve);
     w.D = p; p += 2 * NB * (NB + 4);
-    w.Dinv = p; p += NB;
-    w.lbuf = p; p += 32;
+    w.Dinv = w.D + NB * (NB + 4);
+    w.lbuf = p; p += NB;
     w.sig = sig;
     w.bw = kSolve ? p : nullptr;
     if (kSolve) p += g.nslot;
@@ -90,8 +90,8 @@ pbtrs_cta_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t strid
   w.win = p; p += (size_t)g.nslot * g.lds;
   w.P = p; p += cta_panel_doubles(NB, g, true);
   w.D = p; p += 2 * NB * (NB + 4);
-  w.Dinv = p; p += NB;
-  w.lbuf = p; p += 32;
+  w.Dinv = w.D + NB * (NB + 4);
+  w.lbuf = p; p += NB;
   w.bw = p; p += g.nx;
   w.yb = p;
   w.init_fast();
@@ -193,7 +193,7 @@ bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb, bool solve) {
 // CTAs per SM, else one; 0 if the window does not fit at all.
 int cta_block(int n, int kd, int ldab, bool solve, bcg::CtaGeom* out) {
   const size_t limit = (size_t)smem_optin();
-  const size_t half = 113 * 1024;
+  const size_t half = 113 * 1024 - 512;  // two CTAs per SM: 228 KB less 1 KB per CTA and the static smem
   for (size_t cap : {half, limit}) {
     const int nb = 16;
     bcg::CtaGeom g = make_geom(n, kd, ldab, nb, solve);

@@ -240,7 +240,7 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_solve"
     trace_solve(296)
 
 
-def trace_la(tag, batch=1):
+def trace_la(tag, batch=1, solve=False):
     """Phase breakdown of the pipelined one-CTA factorization (block 0, matrix 0).
 
     Pivot stamps per step: 0 start, 1 after waiting update(k-2), 2 after SYRK(0,0),
@@ -253,24 +253,29 @@ def trace_la(tag, batch=1):
     a = np.concatenate([a] * ((batch + 7) // 8))[:batch]
     a0 = torch.from_numpy(a).cuda()
     nblk = (n + 15) // 16
-    buf = torch.zeros(1 + 8 * (2 * nblk + 4), dtype=torch.int64, device="cuda")
+    buf = torch.zeros(1 + 8 * (3 * nblk + 6), dtype=torch.int64, device="cuda")
     lib = _lib.load()
-    w = a0.clone()
-    bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
-    torch.cuda.synchronize()
+    b0 = torch.from_numpy(np.stack([make_rhs(n, s) for s in range(batch)])).cuda()
+
+    def run():
+        w = a0.clone()
+        if solve:
+            bc.dpbsv_batched_device(w, n, k, k + 1, b0.clone(), batch)
+        else:
+            bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
+        torch.cuda.synchronize()
+    run()
     lib.bcg_set_trace(buf.data_ptr(), buf.numel() * 8)
-    w = a0.clone()
-    bc.dpbtrf_batched_device(w, n, k, k + 1, batch)
-    torch.cuda.synchronize()
+    run()
     lib.bcg_set_trace(None, 0)
     t = buf.cpu().numpy()
     steps = nblk
     allst = t[1:].reshape(-1, 8).astype(np.float64)
     st = allst[:nblk][2:-2]
-    wt = allst[nblk + 1: 2 * nblk + 1][2:-2]
+    wt = allst[2 * nblk + 2: 3 * nblk + 2][2:-2]
     wmed = lambda a, b: float(np.median(wt[:, b] - wt[:, a]))  # noqa: E731
     med = lambda a, b: float(np.median(st[:, b] - st[:, a]))  # noqa: E731  (SM cycles)
-    out = {"config": tag, "batch": batch, "steps": steps, "unit": "cycles",
+    out = {"config": tag, "batch": batch, "solve": solve, "steps": steps, "unit": "cycles",
            "wait_W": med(0, 1), "syrk": med(1, 2), "potrf": med(2, 3), "wait_W1": med(3, 4),
            "trsm_signal": med(4, 5), "worker_wake": med(5, 6), "worker_step": med(6, 7),
            "step": float(np.median(np.diff(st[:, 0]))),
@@ -280,6 +285,7 @@ def trace_la(tag, batch=1):
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_la":
-    trace_la("C1", 1)
     trace_la("C5", 1)
     trace_la("C5", 296)
+    trace_la("C5", 1, True)
+    trace_la("C5", 296, True)
