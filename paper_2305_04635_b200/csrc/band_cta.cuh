@@ -181,15 +181,18 @@ struct CtaGeom {
 
 // The panel buffer P; the backward sweep reuses it for two L11^-1 blocks.
 __host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom& g, bool solve) {
-  // backward: two L11^-1 blocks + the far partial sums ((kCtaThreads - 64) doubles)
-  const size_t p = (size_t)nb_block * g.pld, inv = 2 * (size_t)nb_block * (nb_block + 4) + 192;
+  // backward sweep scratch: 3 x (M_b, G_b) + far partials + c + 2 t, of which the two D
+  // buffers that follow P in shared memory hold 2 * nb_block * (nb_block + 4) doubles
+  const size_t p = (size_t)nb_block * g.pld;
+  const size_t need = 6 * (size_t)nb_block * (nb_block + 4) + 192 + 4 * (size_t)nb_block;
+  const size_t inv = need - 2 * (size_t)nb_block * (nb_block + 4);
   return (solve && inv > p) ? inv : p;
 }
 
-// Column-block buffers of the streamed sweeps: kDepth (4) blocks in flight + the current.
+// Column-block buffers of the streamed sweeps (at most 7, at least 5: host geometry).
 __host__ __device__ inline int cta_sweep_buffers(int nb_block, const CtaGeom& g) {
   const int n = g.nslot / nb_block;
-  return n < 5 ? n : 5;
+  return n < 7 ? n : 7;
 }
 
 // Shared-memory footprint (bytes) of one CTA for block size NB.
@@ -1247,23 +1250,64 @@ struct CtaBand {
     __syncthreads();
   }
 
+  // Backward-sweep inverter (one warp): lane j < 16 solves z^T L_bb = e_j^T (row j of
+  // M = L_bb^-1), lane 16 + j solves z^T L_bb = row j of B (row j of G = B M, B = L(rows of
+  // the next block, cols of this one)); z_k = r_k / L_kk for k = NB-1..0, then
+  // r_i -= z_k L(k, i) for i < k, L entries broadcast from the ring buffer.  Rows go to
+  // out[j*kLDD] (M) and out[NB*kLDD + j*kLDD] (G).  kWhole: every entry in the band.
+  template <bool kWhole>
+  __device__ void invert_bt(const double* blk, int nb, int c0, double* out, double* dsc) const {
+    const int lane = threadIdx.x & 31, j = lane & 15;
+    const bool isg = lane >= 16;
+    if (lane < NB) dsc[lane] = lane < nb ? rcp_nr(blk[lane * g.lds]) : 1.0;
+    double r[NB];
+#pragma unroll
+    for (int kk = 0; kk < NB; ++kk) {
+      const int o = NB + j - kk;  // B(j, kk) = L(c0 + NB + j, c0 + kk)
+      const bool inb = kWhole || (kk < nb && c0 + NB + j < g.n && o <= g.kd);
+      const double bv = blk[kk * g.lds + (inb ? o : 0)];
+      r[kk] = isg ? (inb ? bv : 0.0) : (kk == j ? 1.0 : 0.0);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kk = NB - 1; kk >= 0; --kk) {
+      const double z = r[kk] * dsc[kk];
+      r[kk] = z;
+#pragma unroll
+      for (int i = 0; i < kk; ++i) {
+        if (kWhole) {
+          r[i] = fma(-blk[i * g.lds + kk - i], z, r[i]);
+        } else {
+          const bool inb = kk < nb && kk - i <= g.kd;
+          const double lv = blk[i * g.lds + (inb ? kk - i : 0)];
+          r[i] = fma(inb ? -lv : 0.0, z, r[i]);
+        }
+      }
+    }
+    double* dst = out + (isg ? NB * kLDD : 0) + j * kLDD;
+#pragma unroll
+    for (int kk = 0; kk < NB; kk += 2) *reinterpret_cast<double2*>(dst + kk) = make_double2(r[kk], r[kk + 1]);
+    __syncwarp();
+  }
+
   // Backward sweep L^T x = y (y in rhs after the fused forward sweep).
   //
-  // Block b = columns [b*NB, b*NB+nb): s_j = y_j - sum_{i >= b*NB+nb} L(i,j) x_i, then the
-  // upper-triangular solve L11^T x_b = s.  The sum splits into a "far" part (x of blocks
-  // >= b+2, known one block early) and a "near" part (x of block b+1).  Iteration b runs
-  //   warp 0:     near(b) (16x16 GEMV) + x_b = L11^-T s_b as a product with L11^-1
-  //   warp 1:     L11^-1 of block b-1 (forward substitution, off the critical path)
-  //   warps 2-7:  far(b-1) for the next block, concurrently
-  // so the per-block critical path is two short dot products.  L blocks (and the y
-  // entries) stream in with bulk copies, kDepth blocks ahead, one mbarrier per ring buffer.
+  // Block b = columns [b*NB, b*NB+nb).  With M_b = L_bb^-1, B_b = L(rows of block b+1, cols
+  // of block b) and G_b = B_b M_b:
+  //   x_b = M_b^T (c_b - B_b^T x_{b+1}) = t_b - G_b^T x_{b+1},
+  //   c_b = y_b - sum over rows beyond block b+1 of L(i, block b)^T x_i,  t_b = M_b^T c_b,
+  // so the per-block chain is one 16x16 product.  Iteration b runs
+  //   warp 0 (chain):      x_b = t_b - G_b^T x_{b+1}
+  //   warp 1 (inverter):   rows of M_{b-2} (lanes 0-15) and of G_{b-2} (lanes 16-31): one
+  //                        back substitution z^T L_bb = [e_j | row j of B], same instructions
+  //   warps 2-7 (far):     c_{b-1} (row-parallel partial sums, fixed-order reduction), t_{b-1}
+  // and one CTA barrier.  L blocks (and the y entries) stream in with bulk copies nbuf-1
+  // blocks ahead of their first use (the inverter's), one mbarrier per ring buffer.
   __device__ void backward() {
     const int n = g.n;
     const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
-    constexpr int kDepth = 4;
-    const int nbuf = cta_sweep_buffers(NB, g);  // >= kDepth + 1 (host guarantees nslot >= (kDepth+1)*NB)
+    const int nbuf = cta_sweep_buffers(NB, g);
     const int nblk = (n + NB - 1) / NB;
-    double* sfar = Dinv;            // 2 x NB: far part (incl. y) per block, double-buffered
     const bool bulk_y = fast && !(((uintptr_t)rhs) & 15);
     // parity of the next wait on buffer k's mbarrier, bit k (no divisions in the loop)
     unsigned pbits = 0;
@@ -1296,13 +1340,30 @@ struct CtaBand {
         if (threadIdx.x == 0) mbar_expect_tx(bars + 1 + k, 0);
       }
     };
-    double* li_buf = P;                        // 2 x L11^-1 (the panel buffer is free now)
-    double* part = P + 2 * NB * kLDD;          // far partial sums, kFarChunks x NB
+    // scratch in P (and the D buffers after it): 3 slots of (M_b, G_b), far partials, c, t
+    constexpr int kMG = 2 * NB * kLDD;
     constexpr int kFarThreads = kCtaThreads - 64, kFarChunks = kFarThreads / NB;
-    // far part of block b from x entries of blocks >= b+2 (warps 2-7): thread (chunk q,
-    // column c) sums rows o = o_lo + q, o_lo + q + kFarChunks, ... of column c; the
-    // chunk partials are added in a fixed order (deterministic) after a named barrier.
-    auto far = [&](int b, int k, int sx) {  // k = b % nbuf, sx = ring slot of row b*NB + nb + NB
+    double* mg = P;
+    double* part = P + 3 * kMG;
+    double* cb = part + kFarThreads;  // c of the block in flight (NB)
+    double* tbuf = cb + NB;           // t of two blocks (2 x NB)
+    double* dsc = tbuf + 2 * NB;      // the inverter's pivot reciprocals (NB)
+    auto mslot = [&](int b) { return mg + (b % 3) * kMG; };
+    // inverter: lane j < 16 solves z^T L_bb = e_j^T (row j of M_b), lane 16 + j solves
+    // z^T L_bb = row j of B_b (row j of G_b = B_b M_b); z_k = r_k / L_kk for k = 15..0, then
+    // r_i -= z_k L(k, i) for i < k (L entries broadcast from the ring buffer)
+    auto invert = [&](int b, int k) {
+      const int c0 = b * NB, nb = min(NB, n - c0);
+      const double* blk = win + (size_t)k * NB * g.lds;
+      if (nb == NB && g.kd >= 2 * NB - 1 && c0 + 2 * NB <= n)
+        invert_bt<true>(blk, nb, c0, mslot(b), dsc);
+      else
+        invert_bt<false>(blk, nb, c0, mslot(b), dsc);
+    };
+    // far warps: c_b = y_b - sum_{rows beyond block b+1} L(i, c0+c) x_i (thread (chunk q,
+    // column c) sums rows o_lo + q, + kFarChunks, ...; chunk partials added in a fixed order),
+    // then t_b = M_b^T c_b by the first far warp (lane (i, h): half h of row i's products)
+    auto far_t = [&](int b, int k, int sx) {  // k = b % nbuf, sx = ring slot of row b*NB + nb + NB
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
       const double* blk = win + (size_t)k * NB * g.lds;
@@ -1324,116 +1385,103 @@ struct CtaBand {
       }
       part[q * NB + c] = acc;
       asm volatile("bar.sync 1, %0;" ::"n"(kFarThreads) : "memory");
-      if (t < nb) {
+      if (t < NB) {
         double sum = 0.0;
 #pragma unroll
         for (int qq = 0; qq < kFarChunks; ++qq) sum += part[qq * NB + t];
-        sfar[(b & 1) * NB + t] = yb[k * NB + t] - sum;
+        cb[t] = t < nb ? yb[k * NB + t] - sum : 0.0;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kFarThreads) : "memory");
+      if (t < 32) {
+        const int i = t & 15, h = t >> 4;
+        const double* m = mslot(b) + (8 * h) * kLDD + i;  // M(8h + jj, i)
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += 2) {
+          a0 = fma(m[jj * kLDD], cb[8 * h + jj], a0);
+          a1 = fma(m[(jj + 1) * kLDD], cb[8 * h + jj + 1], a1);
+        }
+        double tv = a0 + a1;
+        tv += __shfl_xor_sync(kFull, tv, 16);
+        if (h == 0) tbuf[(b & 1) * NB + i] = tv;
       }
     };
-    // L11^-1 of block b into buffer b & 1 (warp 1, one block ahead of its use);
-    // li[j*kLDD + i] = Linv(i, j), so warp 0's lane r finds column r contiguous.
-    auto invert = [&](int b, int k) {
-      invert_block<false>(win + (size_t)k * NB * g.lds, min(NB, n - b * NB), li_buf + (b & 1) * NB * kLDD);
+    // chain: x_b = t_b - G_b^T x_{b+1} (lane (i, h): half h of column i of G), to the x ring
+    // and to rhs
+    auto chain = [&](int b, int xb) {  // xb = ring slot of row b*NB
+      const int c0 = b * NB, nb = min(NB, n - c0);
+      const int i = lane & 15, h = lane >> 4;
+      double a0 = 0.0, a1 = 0.0;
+      if (b + 1 < nblk) {
+        const double* G = mslot(b) + NB * kLDD + (8 * h) * kLDD + i;  // G(8h + jj, i)
+        int sx = xb + nb + 8 * h;  // row c0 + nb + 8h
+        if (sx >= g.nx) sx -= g.nx;
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += 2) {
+          int s0 = sx + jj, s1 = sx + jj + 1;
+          if (s0 >= g.nx) s0 -= g.nx;
+          if (s1 >= g.nx) s1 -= g.nx;
+          const int r0 = c0 + nb + 8 * h + jj;
+          const double x0 = r0 < n ? bw[s0] : 0.0, x1 = r0 + 1 < n ? bw[s1] : 0.0;
+          a0 = fma(G[jj * kLDD], x0, a0);
+          a1 = fma(G[(jj + 1) * kLDD], x1, a1);
+        }
+      }
+      double s = a0 + a1;
+      s += __shfl_xor_sync(kFull, s, 16);
+      const double x = tbuf[(b & 1) * NB + i] - s;
+      if (lane < nb) {
+        int sr = xb + lane;
+        if (sr >= g.nx) sr -= g.nx;
+        bw[sr] = x;
+        rhs[c0 + lane] = x;
+      }
     };
     // ring positions, tracked incrementally: kb = block b's buffer, xb = ring slot of row b*NB
+    auto dec = [&](int v, int by, int mod) { v -= by; return v < 0 ? v + mod : v; };
     int kb = (nblk - 1) % nbuf;
     int xb = ((nblk - 1) * NB) % g.nx;
-    auto dec = [&](int v, int by, int mod) { v -= by; return v < 0 ? v + mod : v; };
-    for (int d = 0; d < kDepth; ++d) issue(nblk - 1 - d, dec(kb, d, nbuf));
+    for (int d = 0; d < nbuf; ++d) issue(nblk - 1 - d, dec(kb, d, nbuf));
     const int tb = nblk + 1;  // trace rows after the factorization's
-    // prologue: far part of the last block (nothing beyond it)
+    // prologue: M/G of the last two blocks, c/t of the last one
     wait_buf(kb);
     __syncthreads();
+    if (warp == 1) invert(nblk - 1, kb);
+    __syncthreads();
+    if (nblk >= 2) wait_buf(dec(kb, 1, nbuf));
+    __syncthreads();
+    if (warp == 1 && nblk >= 2) invert(nblk - 2, dec(kb, 1, nbuf));
     if (warp >= 2) {
       const int nbl = n - (nblk - 1) * NB;
       int sx = xb + nbl + NB;
       while (sx >= g.nx) sx -= g.nx;
-      far(nblk - 1, kb, sx);
-    } else if (warp == 1) {
-      invert(nblk - 1, kb);
+      far_t(nblk - 1, kb, sx);
     }
+    __syncthreads();
+    issue(nblk - 1 - nbuf, kb);  // the last block is done (inverter, far): its buffer moves on
     for (int b = nblk - 1; b >= 0; --b) {
-      const int k = kb, km1 = dec(kb, 1, nbuf);
-      const int c0 = b * NB;
-      const int nb = min(NB, n - c0);
+      const int km1 = dec(kb, 1, nbuf), km2 = dec(kb, 2, nbuf);
       if (threadIdx.x < 32) trace_stamp(tb + b, 0);
-      if (b >= 1) wait_buf(km1);  // block b-1, per thread
-      // far(b), L11^-1(b) and x of block b+1 were published by the previous iteration's
-      // closing barrier; only the prologue's far/invert needs one here
-      if (b == nblk - 1) __syncthreads();
+      if (b >= 2) wait_buf(km2);  // block b-2 (the inverter's), per thread
       if (threadIdx.x < 32) trace_stamp(tb + b, 1);
       if (warp == 0) {
-        const double* blk = win + (size_t)k * NB * g.lds;
-        const int r = lane;
-        double v = r < nb ? sfar[(b & 1) * NB + r] : 0.0;
-        if (r < nb) {
-          // near part: rows c0+nb .. c0+nb+NB-1 (block b+1), in band for this column
-          const double* colr = blk + r * g.lds;
-          const int len = col_len(c0 + r);
-          int sx = xb + nb;
-          if (sx >= g.nx) sx -= g.nx;
-          double a0 = 0.0, a1 = 0.0;
-          if (nb == NB && nb - r + NB - 1 < len && sx + NB <= g.nx) {  // in band, no ring wrap
-            const double* xs = bw + sx;
-#pragma unroll
-            for (int t = 0; t < NB; t += 2) {
-              a0 = fma(colr[nb - r + t], xs[t], a0);
-              a1 = fma(colr[nb - r + t + 1], xs[t + 1], a1);
-            }
-          } else {
-#pragma unroll
-            for (int t = 0; t < NB; t += 2) {
-              const int o0 = nb - r + t, o1 = o0 + 1;
-              int s0i = sx + t, s1i = sx + t + 1;
-              if (s0i >= g.nx) s0i -= g.nx;
-              if (s1i >= g.nx) s1i -= g.nx;
-              if (o0 < len) a0 = fma(colr[o0], bw[s0i], a0);
-              if (o1 < len) a1 = fma(colr[o1], bw[s1i], a1);
-            }
-          }
-          v -= a0 + a1;
-        }
-        // x_b = L11^-T s_b: lane r dots column r of L11^-1 with s (no sequential chain)
-        double* ss = Dinv + 2 * NB;
-        if (r < NB) ss[r] = v;
-        __syncwarp();
-        const double* li = li_buf + (b & 1) * NB * kLDD + (r < NB ? r : 0) * kLDD;
-        double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-        for (int c = 0; c < NB; c += 4) {
-          const double2 l01 = *reinterpret_cast<const double2*>(li + c);
-          const double2 l23 = *reinterpret_cast<const double2*>(li + c + 2);
-          const double2 s01 = *reinterpret_cast<const double2*>(ss + c);
-          const double2 s23 = *reinterpret_cast<const double2*>(ss + c + 2);
-          x0 = fma(l01.x, s01.x, x0);
-          x1 = fma(l01.y, s01.y, x1);
-          x0 = fma(l23.x, s23.x, x0);
-          x1 = fma(l23.y, s23.y, x1);
-        }
-        v = x0 + x1;
-        __syncwarp();
-        if (r < nb) {
-          int sr = xb + r;
-          if (sr >= g.nx) sr -= g.nx;
-          bw[sr] = v;
-          rhs[c0 + r] = v;
-        }
+        chain(b, xb);
         trace_stamp(tb + b, 2);
+        // block b is done (far at b+1, inverter at b+2): its buffer takes block b - nbuf, issued
+        // here by the chain warp (it has slack) rather than after the barrier
+        if (fast && b <= nblk - 2) issue(b - nbuf, kb);
+      } else if (warp == 1) {
+        if (b >= 2) invert(b - 2, km2);
+        trace_stamp(tb + b, 4);
       } else if (b >= 1) {
-        if (warp >= 2) {
-          int sxf = xb + NB;  // row (b-1)*NB + NB + NB = c0 + NB
-          if (sxf >= g.nx) sxf -= g.nx;
-          far(b - 1, km1, sxf);
-          if (warp == 2) trace_stamp(tb + b, 5);
-        } else {
-          invert(b - 1, km1);
-          trace_stamp(tb + b, 4);
-        }
+        int sxf = xb + NB;  // row (b-1)*NB + NB + NB = c0 + NB
+        if (sxf >= g.nx) sxf -= g.nx;
+        far_t(b - 1, km1, sxf);
+        if (warp == 2) trace_stamp(tb + b, 5);
       }
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(tb + b, 3);
-      issue(b - kDepth, dec(kb, kDepth, nbuf));  // block b+1's buffer is free now
+      if (!fast && b <= nblk - 2) issue(b - nbuf, kb);  // element-wise fallback: all threads
       kb = km1;
       xb = dec(xb, NB, g.nx);
     }

@@ -321,13 +321,16 @@ int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t s
   return cuda_status(cudaGetLastError(), "pbtrs_after_factor_kernel launch");
 }
 
-// Streamed solve (shared-memory ring of 5 column blocks) when it fits, else the
+// Streamed solve (shared-memory ring of 5-7 column blocks) when it fits, else the
 // direct-from-L2 kernel.
 static int launch_solve(const double* ab, int64_t sab, double* b, int64_t sb, int nrhs, int64_t blocks, int n,
                         int kd, int ldab, int32_t* info, cudaStream_t st) {
   bcg::CtaGeom g = make_geom(n, kd, ldab, 16, true);
-  g.nslot = 5 * 16;                 // block buffers for the streamed sweeps
   g.nx = ((kd + 48) + 1) & ~1;      // rows in flight: kd + NB, plus the entering block
+  // block buffers for the streamed sweeps: 7 (deeper prefetch) when two CTAs still fit per
+  // SM, else 5
+  g.nslot = 7 * 16;
+  if (bcg::cta_smem_bytes(16, g, true) > (size_t)(113 * 1024 - 512)) g.nslot = 5 * 16;
   const size_t smem = bcg::cta_smem_bytes(16, g, true);
   if (smem <= (size_t)smem_optin()) {
     auto k = bcg::pbtrs_cta_kernel;
