@@ -878,13 +878,15 @@ struct CtaBand {
       if (m > NB) trsm_panel(s0, j0, nb, m, 1 + wk, kWorkers, kSolve);
       fence_async_smem();
       if (wk == 0) trace_stamp(tw, 3);
-      named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete (+ the light warp)
-      if (wk == 0) trace_stamp(tw, 4);
+      // tile column 0 of update(k) (the next panel): tile (t, 0) needs only this warp's own
+      // TRSM tile X_t and the pivot's X_0, so it runs before barrier B
       const int T = (m + 15) >> 4;
-      update_tiles(s0, j0, nb, m, 1, T, wk, kWorkers);  // tile column 0 (the next panel)
+      __syncwarp();
+      update_tiles(s0, j0, nb, m, 1, T, wk, kWorkers);
       __syncwarp();
       if (lane == 0) mbar_arrive(sig + 1);
-      // forward sweep: rows of panel tiles 1.. lose X y_k
+      if (wk == 0) trace_stamp(tw, 4);
+      named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete (+ the light warp)
       if (wk == 0) trace_stamp(tw, 5);
       // the rest, starting with the workers that had no column-0 tile
       const int first = (T - 1) % kWorkers;
@@ -905,6 +907,8 @@ struct CtaBand {
       const int j0 = k * NB, nb = min(NB, n - j0);
       mbar_wait(sig, k & 1);
       if (*s_fail >= 0) break;
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(sig + 1);
       if (kSolve) cp_async_wait_all();  // rhs entries of the rows the previous prefetch brought in
       named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete
       light_store(j0, nb, s0);
@@ -926,7 +930,10 @@ struct CtaBand {
     init_fast();
     for (int idx = threadIdx.x; idx < NB * g.pld; idx += kCtaThreads) P[idx] = 0.0;
     if (threadIdx.x == 0) {
-      for (int i = 0; i < 4; ++i) mbar_init(sig + i, i == 0 ? 1 : kWorkers);
+      // sig[1] (column 0 done) also counts the light warp's arrival right after it consumed
+      // sig[0]: the workers arrive before barrier B, so without it the pivot could complete
+      // sig[0] twice before the light warp waited once
+      for (int i = 0; i < 4; ++i) mbar_init(sig + i, i == 0 ? 1 : (i == 1 ? kWorkers + 1 : kWorkers));
       s_fail = -1;
       s_nload = 0;
     }
