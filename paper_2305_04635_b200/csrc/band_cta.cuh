@@ -134,6 +134,13 @@ __device__ __forceinline__ double shfl_early(double v, int src) {
   return r;
 }
 
+// Column permutation of the tile GEMM's B operand / C fragment: lane (gr, gc) loads B column
+// kPerm(gr) and owns C columns kPerm(2gc), kPerm(2gc+1).  With column strides = 4 (mod 16)
+// doubles (window lds - 1 = 100 for kd = 100, P's pld, D's kLDD) every fragment access of a
+// half-warp -- B loads and the C loads/stores in the band window or P -- hits 16 distinct
+// bank pairs (the identity order makes the C accesses 2-way conflicted).
+__device__ __forceinline__ int kperm(int x) { return (0x57463120u >> (4 * x)) & 7; }  // 0,2,1,3,6,4,7,5
+
 // d -= a b (negated A operand; not volatile, so the scheduler may interleave chains)
 __device__ __forceinline__ void dmma884n(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -615,7 +622,7 @@ struct CtaBand {
     constexpr bool kU1 = ROWS != 2;   // rows i0+8.. computed
     constexpr bool kV1 = !DIAG;       // block (0,1) computed
     auto ok = [&](int u, int v, int e) {
-      const int i = i0 + u * 8 + gr, q = q0 + v * 8 + 2 * gc + e;
+      const int i = i0 + u * 8 + gr, q = q0 + v * 8 + kperm(2 * gc + e);
       bool r = true;
       if (DIAG && u == v) r = q <= i;
       if (ROWS != 0 && (u == 1 || ROWS == 2)) r = r && i < m;
@@ -636,7 +643,7 @@ struct CtaBand {
     for (int k0 = 0; k0 < NB; k0 += 4) {
       const double* pk = P + (k0 + gc) * g.pld;
       const double a0 = pk[i0 + gr], a1 = kU1 ? pk[i0 + 8 + gr] : 0.0;
-      const double b0 = pk[q0 + gr], b1 = pk[q0 + 8 + gr];
+      const double b0 = pk[q0 + kperm(gr)], b1 = pk[q0 + 8 + kperm(gr)];
       dmma884n(acc[0][0][0], acc[0][0][1], a0, b0);
       if (kU1) dmma884n(acc[1][0][0], acc[1][0][1], a1, b0);
       if (kV1) dmma884n(acc[0][1][0], acc[0][1][1], a0, b1);
@@ -673,7 +680,7 @@ struct CtaBand {
       for (int v = 0; v < 2; ++v)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int q = q0 + v * 8 + 2 * gc + e;
+          const int q = q0 + v * 8 + kperm(2 * gc + e);
           cb[v][e] = slot_from(s0, j0, base + (q < m ? q : 0)) * g.lds - q;
         }
       const int rows = i0 + 16 <= m ? 0 : (i0 + 8 < m ? 1 : 2);
