@@ -557,7 +557,7 @@ struct CtaBand {
           a[u] = in ? v : 0.0;
         }
 #pragma unroll
-        for (int v = 0; v < NB / 8; ++v) bf[v] = D[(8 * v + gr) * kLDD + k];
+        for (int v = 0; v < NB / 8; ++v) bf[v] = D[(8 * v + kperm(gr)) * kLDD + k];  // (kperm: conflict-free C)
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -572,7 +572,7 @@ struct CtaBand {
         for (int v = 0; v < NB / 8; ++v)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int c = 8 * v + 2 * gc + e;
+            const int c = 8 * v + kperm(2 * gc + e);
             const int off = nb + r - c;
             const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
             P[c * g.pld + r] = acc[u][v][e];
