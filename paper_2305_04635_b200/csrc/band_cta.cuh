@@ -1378,34 +1378,45 @@ struct CtaBand {
     // column c) sums rows o_lo + q, + kFarChunks, ...; chunk partials added in a fixed order),
     // then t_b = M_b^T c_b by the first far warp (lane (i, h): half h of row i's products)
     auto far_t = [&](int b, int k, int sx) {  // k = b % nbuf, sx = ring slot of row b*NB + nb + NB
+      // (tensor path: sum_rows L(row, c0 + col) x_row is a 16 x R by R x 1 product, k-steps of
+      // four rows dealt round-robin to the six warps, x in column 0 of B; the six partial
+      // columns are added in a fixed order, so the result is deterministic)
       const int c0 = b * NB;
       const int nb = min(NB, n - c0);
       const double* blk = win + (size_t)k * NB * g.lds;
       const int rlo = c0 + nb + NB;  // first row of block b+2
+      const int rhi = min(n - 1, c0 + nb - 1 + g.kd);
       const int t = threadIdx.x - 64;
-      const int c = t % NB, q = t / NB;
-      double acc = 0.0;
-      if (c < nb) {
-        const int j = c0 + c;
-        const int len = col_len(j);
-        const double* colj = blk + c * g.lds;
-        int sl = sx + q;
+      const int fw = t >> 5, gr = lane >> 2, gc = lane & 3;
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      const int nks = rhi >= rlo ? (rhi - rlo + 4) >> 2 : 0;
+      for (int ks = fw; ks < nks; ks += kFarThreads / 32) {
+        const int row = rlo + 4 * ks + gc;
+        int sl = sx + 4 * ks + gc;
         if (sl >= g.nx) sl -= g.nx;
-        for (int o = rlo - j + q; o < len; o += kFarChunks) {
-          acc = fma(colj[o], bw[sl], acc);
-          sl += kFarChunks;
-          if (sl >= g.nx) sl -= g.nx;
+        const double xv = (gr == 0 && row <= rhi) ? bw[sl] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int col = 8 * u + gr;
+          const int off = row - c0 - col;
+          const bool in = col < nb && row <= rhi && off <= g.kd;
+          const double av = blk[col * g.lds + (in ? off : 0)];
+          dmma884(acc[u][0], acc[u][1], in ? av : 0.0, xv);
         }
       }
-      part[q * NB + c] = acc;
-      asm volatile("bar.sync 1, %0;" ::"n"(kFarThreads) : "memory");
-      if (t < NB) {
-        double sum = 0.0;
-#pragma unroll
-        for (int qq = 0; qq < kFarChunks; ++qq) sum += part[qq * NB + t];
-        cb[t] = t < nb ? yb[k * NB + t] - sum : 0.0;
+      if (gc == 0) {
+        part[fw * NB + gr] = acc[0][0];
+        part[fw * NB + 8 + gr] = acc[1][0];
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kFarThreads) : "memory");
+      if (t < 32) {
+        const int i = t & 15;
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kFarThreads / 32; ++w) sum += part[w * NB + i];
+        if (t < NB) cb[t] = t < nb ? yb[k * NB + t] - sum : 0.0;
+        __syncwarp();
+      }
       if (t < 32) {
         const int i = t & 15, h = t >> 4;
         const double* m = mslot(b) + (8 * h) * kLDD + i;  // M(8h + jj, i)
