@@ -197,7 +197,8 @@ __host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom&
 }
 
 // Column-block buffers of the streamed sweeps (at most 7, at least 5: host geometry).
-__host__ __device__ inline int cta_sweep_buffers(int nb_block, const CtaGeom& g) {
+template <class G>
+__host__ __device__ inline int cta_sweep_buffers(int nb_block, const G& g) {
   const int n = g.nslot / nb_block;
   return n < 7 ? n : 7;
 }
@@ -211,10 +212,32 @@ __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g,
   return d * sizeof(double) + 64;
 }
 
-template <int NB, bool kSolve>
+// Compile-time geometry for one band width (the bench configuration): kd, ldab = lds =
+// kd + 1, the ring and panel strides exactly as make_geom() (bandchol_b200.cu) picks them,
+// so index arithmetic folds to constants and frees registers in the hot loops; n stays
+// runtime.  KD = 0 selects the runtime CtaGeom.
+template <int KD, bool kSolve>
+struct GeomFixed {
+  int n;
+  static constexpr int kd = KD, ldab = KD + 1, lds = KD + 1;
+  static constexpr int ns0 = (kSolve && KD + 16 < 5 * 16) ? 5 * 16 : KD + 16;
+  static constexpr int nslot = (ns0 & 1) ? ns0 + 1 : ns0, nx = nslot;
+  static constexpr int pld = KD + ((4 - KD % 16) + 16) % 16;
+  __host__ __device__ GeomFixed(const CtaGeom& x) : n(x.n) {}
+  // true when the runtime geometry the host chose is exactly this one
+  __host__ __device__ static bool matches(const CtaGeom& x) {
+    return x.kd == kd && x.ldab == ldab && x.lds == lds && x.nslot == nslot && x.nx == nx && x.pld == pld;
+  }
+};
+template <int KD, bool kSolve>
+struct GeomOf { using type = GeomFixed<KD, kSolve>; };
+template <bool kSolve>
+struct GeomOf<0, kSolve> { using type = CtaGeom; };
+
+template <int NB, bool kSolve, int KD = 0>
 struct CtaBand {
   static_assert(NB == 16, "block size: lanes 16-31 of the POTRF warp invert L11");
-  const CtaGeom g;
+  const typename GeomOf<KD, kSolve>::type g;
   double* __restrict__ ab;   // this matrix in global memory
   double* __restrict__ rhs;  // its right-hand side (kSolve)
   double* win;               // shared ring of column slots
