@@ -5,7 +5,8 @@ independent SPD band matrices n=4096, kd=100, factor + one-RHS band solve per ma
 the one config that partitions across GPUs (each rank factors its own batch of
 1,024 matrices with distinct seeds, no collective on the data path; per-GPU work is
 fixed as N grows => "weak" scaling, value = matrices of all ranks / max-over-ranks time).  `--config C1..C4` benches a single-matrix
-config instead.  A step = one fused factor+solve pass over the whole batch (C5) or one
+config instead.  A step = one factor+solve pass over the whole batch (C5: bcg_dpbsv_batched,
+i.e. the pipelined factorization kernel then the streamed solve kernel) or one
 factorization (+ solve for C2) of the matrix, inputs resident in HBM; a fresh
 device-to-device copy of the pristine inputs is made before every step OUTSIDE the
 timed events (it also flushes L2: 3.4 GB > 126 MB).
@@ -284,7 +285,9 @@ def run_gpu_arm(args) -> int:
     def step():
         if cfg.batch > 1:
             bc.dpbsv_batched_device(work_a, n, kd, ld, work_b, nb, info=info, stream=stream)
-            return 1
+            # bcg_dpbsv_batched: kd >= 32 runs the pipelined factorization, then the streamed
+            # solve (two kernels); narrower bands one fused kernel
+            return 2 if kd >= 32 else 1
         bc.dpbtrf_device(work_a[0], n, kd, ld, info=info, stream=stream)
         if cfg.solve:
             bc.dpbtrs_device(work_a[0], n, kd, ld, work_b[0], info=info, stream=stream)
