@@ -1141,6 +1141,7 @@ struct CtaBand {
     const int nbuf = cta_sweep_buffers(NB, g);
     const int nblk = (n + NB - 1) / NB;
     double* ycur = Dinv;  // y of the last two blocks (2 x NB)
+    const bool early_issue = fast && nbuf >= kDepth + 3;
     double* li_buf = P;
     // parity of the next wait on buffer k (bit k) and ring positions, tracked without divisions
     unsigned pbits = 0;
@@ -1237,6 +1238,9 @@ struct CtaBand {
           rhs[c0 + r] = v;
         }
         trace_stamp(b, 2);
+        // with >= kDepth + 3 buffers the slot block b + kDepth goes to (block b-3's) is already
+        // free: the chain warp issues it now rather than after the barrier
+        if (early_issue) issue(b + kDepth, inc(kb, kDepth, nbuf));
       } else if (warp == 1) {
         if (b + 1 < nblk) invert(b + 1, kp1);
         trace_stamp(b, 4);
@@ -1273,7 +1277,7 @@ struct CtaBand {
       }
       __syncthreads();
       if (threadIdx.x < 32) trace_stamp(b, 3);
-      issue(b + kDepth, inc(kb, kDepth, nbuf));  // block b-1's buffer is free now
+      if (!early_issue) issue(b + kDepth, inc(kb, kDepth, nbuf));  // block b-1's buffer is free now
       kb = kp1;
       xb = inc(xb, NB, g.nx);
     }
