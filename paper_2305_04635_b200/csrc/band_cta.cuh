@@ -553,9 +553,7 @@ struct CtaBand {
   // warps, DMMA m8n8k4 with A from the window (entries outside the band read as 0) and
   // B(k, c) = Linv(c, k) from D.  X goes to the dense panel P and back to the window.
   // Tiles t = wid, wid + nw, ... (the calling warp is worker wid of nw).
-  // rhs: also b(rows of the tile) -= X y (y = this step's forward-sweep block in yb) as
-  // DMMA with y in column 0 of B, so no scalar FP64 chain runs on a DMMA-busy SMSP.
-  __device__ void trsm_panel(int s0, int j0, int nb, int m, int wid, int nw, bool rhs = false) {
+  __device__ void trsm_panel(int s0, int j0, int nb, int m, int wid, int nw) {
     const int lane = threadIdx.x & 31;
     const int gr = lane >> 2, gc = lane & 3;
     const int sw = g.nslot - s0;
@@ -601,30 +599,6 @@ struct CtaBand {
             P[c * g.pld + r] = acc[u][v][e];
             if (c < nb && off <= g.kd) win[sl * g.lds + off] = acc[u][v][e];
           }
-      }
-      if (kSolve && rhs) {
-        __syncwarp();  // X of this tile in P (A operand); B(kk, n) = y_kk for n == 0
-        const double* y = yb + ((j0 / NB) & 1) * NB;
-        double cr[2][2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int r = 16 * t + 8 * u + gr;
-          cr[u][0] = (gc == 0 && r < m) ? bw[slot_from(s0, j0, j0 + nb + r)] : 0.0;
-          cr[u][1] = 0.0;
-        }
-#pragma unroll
-        for (int kk = 0; kk < NB / 4; ++kk) {
-          const int k = 4 * kk + gc;
-          const double bfr = (gr == 0 && k < nb) ? y[k] : 0.0;
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-            if (u == 0 || !tail) dmma884n(cr[u][0], cr[u][1], P[k * g.pld + 16 * t + 8 * u + gr], bfr);
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int r = 16 * t + 8 * u + gr;
-          if (gc == 0 && r < m) bw[slot_from(s0, j0, j0 + nb + r)] = cr[u][0];
-        }
       }
     }
   }
@@ -738,8 +712,8 @@ struct CtaBand {
 
   // ---- pipelined factorization (kd >= 32) -------------------------------------------
   // Three warp roles, no CTA-wide barrier inside the column loop:
-  //   pivot (SMSP 0): SYRK of tile (0,0) of update(k-1) -> POTRF(k) (+ L11^-1, + forward
-  //                   sweep) -> TRSM of panel tile 0 -> signal sig[0] ("panel k ready")
+  //   pivot (SMSP 0): SYRK of tile (0,0) of update(k-1) -> POTRF(k) (+ L11^-1) -> TRSM of
+  //                   panel tile 0 -> signal sig[0] ("panel k ready")
   //   workers (6, SMSPs 1-3): TRSM of panel tiles 1.. -> column 0 of update(k) (signal
   //                   sig[1]) -> the rest of update(k) (signal sig[2 + (k&1)])
   //   light (SMSP 0): write-back of panel k, prefetch of the columns update(k+1) needs
@@ -769,7 +743,7 @@ struct CtaBand {
     }
     __syncwarp();
   }
-  // light warp: columns [jlo, jhi) (+ their rhs entries) into the ring from slot sj on;
+  // light warp: columns [jlo, jhi) into the ring from slot sj on;
   // completes one phase of bars[0]
   __device__ void light_load(int jlo, int jhi, int sj) {
     const int lane = threadIdx.x & 31;
@@ -788,53 +762,8 @@ struct CtaBand {
         for (int o = lane; o < g.ldab; o += 32) win[sl * g.lds + o] = ab[(int64_t)j * g.ldab + o];
       }
     }
-    if (kSolve) {  // rhs entries: cp.async, completed before the next barrier B (light_loop)
-      for (int j = jlo + lane; j < jhi; j += 32) cp_async8(bw + slot_from(sj, jlo, j), rhs + j);
-      cp_async_commit();
-    }
     __syncwarp();
     if (!fast && lane == 0) mbar_arrive(bars);  // plain arrival: completes the phase
-  }
-
-  // Fused solve, pivot warp: y_k = L11^-1 s_k once L11^-1 is in D (a 16 x 16 product: two
-  // half rows per lane, 4-deep chains; the substitution inside the POTRF loop would add a
-  // shuffle chain to every column), to rhs (global, for the backward sweep) and yb.
-  __device__ void forward_block(int k, int j0, int nb, int s0) {
-    const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
-    const double* li = D + r * kLDD + 8 * h;  // Linv(r, 8h..), row-major
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; t += 2) {
-      const int j = 8 * h + t;
-      const double s0v = j < nb ? bw[slot_from(s0, j0, j0 + j)] : 0.0;
-      const double s1v = j + 1 < nb ? bw[slot_from(s0, j0, j0 + j + 1)] : 0.0;
-      a0 = fma(li[t], s0v, a0);
-      a1 = fma(li[t + 1], s1v, a1);
-    }
-    double y = a0 + a1;
-    y += __shfl_down_sync(kFull, y, 16);
-    if (lane < nb) {
-      rhs[j0 + lane] = y;
-      yb[(k & 1) * NB + lane] = y;
-    }
-    __syncwarp();
-  }
-
-  // Fused solve, pivot warp: block k+1's rhs rows lose X0(k) y_k (X0 in P rows 0..15, y_k in
-  // yb).  Lane (r, h) sums half h of row r's products; the halves meet by shuffle.
-  __device__ void rhs_next_block(int k, int j0, int nb, int m, int s0) {
-    const int lane = threadIdx.x & 31, r = lane & 15, h = lane >> 4;
-    const double* y = yb + (k & 1) * NB + 8 * h;
-    double b0 = 0.0, b1 = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; t += 2) {
-      b0 = fma(P[(8 * h + t) * g.pld + r], y[t], b0);
-      b1 = fma(P[(8 * h + t + 1) * g.pld + r], y[t + 1], b1);
-    }
-    double u = b0 + b1;
-    u += __shfl_down_sync(kFull, u, 16);
-    if (lane < min(NB, m)) bw[slot_from(s0, j0, j0 + nb + lane)] -= u;
-    __syncwarp();
   }
 
   __device__ void pivot_loop(int nblk, volatile int* s_fail) {
@@ -855,7 +784,6 @@ struct CtaBand {
       trace_stamp(k, 2);
       D = Dbase + (k & 1) * NB * kLDD;
       const int f = potrf_diag<false>(s0, j0, nb);
-      if (kSolve && f < 0) forward_block(k, j0, nb, s0);
       trace_stamp(k, 3);
       // column 0 of update(k-1) done: A(k+1, k) is final and P rows 0..15 are free.  Also
       // waited when there is no TRSM (last block, failure): it proves every worker and the
@@ -872,9 +800,6 @@ struct CtaBand {
       fence_async_smem();  // L11 and X0 in the window -> the light warp's bulk write-back
       __syncwarp();
       if (lane == 0) mbar_arrive(sig);
-      // block k+1's rhs rows (read by POTRF(k+1)); P rows 0..15 stay X0(k) until this
-      // warp's next TRSM
-      if (kSolve && m > 0) rhs_next_block(k, j0, nb, m, s0);
       trace_stamp(k, 5);
       sp = s0;
       mp = m;
@@ -904,8 +829,7 @@ struct CtaBand {
       named_bar(kBarA, 32 * kWorkers);  // update(k-1) done by every worker
       if (wk == 0) trace_stamp(tw, 2);
       D = Dbase + (k & 1) * NB * kLDD;
-      // (fused solve: each TRSM tile also takes X y_k off its rhs rows, on the tensor path)
-      if (m > NB) trsm_panel(s0, j0, nb, m, 1 + wk, kWorkers, kSolve);
+      if (m > NB) trsm_panel(s0, j0, nb, m, 1 + wk, kWorkers);
       fence_async_smem();
       if (wk == 0) trace_stamp(tw, 3);
       // tile column 0 of update(k) (the next panel): tile (t, 0) needs only this warp's own
@@ -939,7 +863,6 @@ struct CtaBand {
       if (*s_fail >= 0) break;
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(sig + 1);
-      if (kSolve) cp_async_wait_all();  // rhs entries of the rows the previous prefetch brought in
       named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete
       light_store(j0, nb, s0);
       const int jlo = j0 + NB + kd;
@@ -977,7 +900,6 @@ struct CtaBand {
       worker_loop(nblk, &s_fail);
     } else {
       const int nload = light_loop(nblk, &s_fail);
-      if (kSolve) cp_async_wait_all();
       if ((threadIdx.x & 31) == 0) {
         s_nload = nload;
         if (nload > 0) mbar_wait(bars, phase ^ ((unsigned)(nload - 1) & 1u));  // the last prefetch landed
@@ -994,9 +916,12 @@ struct CtaBand {
     return fail < 0 ? -1 : fail;
   }
 
-  // Whole factorization (+ forward sweep when kSolve).  Returns -1 or failing column.
+  // Whole factorization (+ forward sweep when kSolve, lock-step loop only).  Returns -1 or
+  // the failing column.
   __device__ int factor() {
-    if (g.kd >= 32) return factor_la();
+    // (the fused solve runs the lock-step loop below: for kd >= 32 bcg_dpbsv_batched factors with
+    // the pipelined kernel and then runs the streamed solve, which measured faster)
+    if (!kSolve && g.kd >= 32) return factor_la();
     const int n = g.n, kd = g.kd;
     __shared__ int s_fail;
     const int warp = threadIdx.x >> 5;
@@ -1331,7 +1256,7 @@ struct CtaBand {
     __syncwarp();
   }
 
-  // Backward sweep L^T x = y (y in rhs after the fused forward sweep).
+  // Backward sweep L^T x = y (y in rhs after the forward sweep).
   //
   // Block b = columns [b*NB, b*NB+nb).  With M_b = L_bb^-1, B_b = L(rows of block b+1, cols
   // of block b) and G_b = B_b M_b:
