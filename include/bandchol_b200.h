@@ -67,11 +67,12 @@ int bcg_dpbtrs(int64_t n, int64_t kd, const double* ab, int64_t ldab, double* b,
 int bcg_dpbtrs_batched(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab,
                        double* b, int64_t stride_b, int64_t batch, int32_t* info, void* stream);
 
-/* Fused batched factor + forward sweep + backward sweep (factor and solve of
- * config C5 in one launch per matrix group): on return ab holds L and b holds
- * x.  info: device int32[batch] with the dpbtrf convention; when a matrix fails
- * its ab and b contents are unspecified (as after a failed reference factorization,
- * which leaves the matrix partially overwritten). */
+/* Batched factor + solve (config C5): on return ab holds L and b holds x.  Stream-ordered on
+ * `stream`; for kd >= 32 it launches the pipelined factorization and then the streamed
+ * two-sweep solve (which skips failed matrices), for narrower bands one fused kernel.
+ * info: device int32[batch] with the dpbtrf convention; when a matrix fails its ab and b
+ * contents are unspecified (as after a failed reference factorization, which leaves the
+ * matrix partially overwritten). */
 int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab,
                       double* b, int64_t stride_b, int64_t batch, int32_t* info, void* stream);
 

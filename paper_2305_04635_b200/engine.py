@@ -165,7 +165,8 @@ def dpbtrs_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=No
 
 
 def dpbsv_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=None, stream=None):
-    """Fused factor + solve of `batch` systems: ab -> L, b -> x, one launch."""
+    """Factor + solve of `batch` systems: ab -> L, b -> x (bcg_dpbsv_batched: for kd >= 32 the
+    pipelined factorization then the streamed solve, else one fused kernel)."""
     torch = _torch()
     _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
     _dev(b, torch, torch.float64, n * batch, "b")
@@ -362,7 +363,7 @@ _pinned_keepalive: dict = {}
 
 
 class BatchedBandSolver:
-    """Device-resident workspace for repeated fused factor + solve of a fixed-shape batch.
+    """Device-resident workspace for repeated factor + solve of a fixed-shape batch.
 
     `factor_solve(ab_host, b_host)` copies the batch in, factors every matrix and
     solves its system (bcg_dpbsv_batched), and copies L and x back into the same
