@@ -93,3 +93,20 @@ def test_pipelined_odd_shapes_factor_and_solve(n, k, ld):
     assert np.array_equal(out[pad], data[0][pad])  # padding untouched
     xs = oracle.solve(n, k, ld, want, b[0])
     assert np.linalg.norm(dvb.cpu().numpy()[0] - xs) <= X_TOL * np.linalg.norm(xs)
+
+
+def test_compile_time_geometry_matches_runtime_geometry():
+    """kd = 100 with ldab = 101 runs the GeomFixed<100> instantiation, a padded ldab the runtime
+    one: the same arithmetic in the same order, so L must agree bit for bit."""
+    n, k, B = 1200, 100, 5
+    data = np.stack([generate_spd(n, k, s).data for s in range(B)])
+    a = torch.from_numpy(data.copy()).cuda()
+    assert int(bc.dpbtrf_batched_device(a, n, k, k + 1, B).abs().sum().item()) == 0
+    ld = k + 3
+    padded = np.zeros((B, ld * n))
+    padded.reshape(B, n, ld)[:, :, :k + 1] = data.reshape(B, n, k + 1)
+    p = torch.from_numpy(padded).cuda()
+    assert int(bc.dpbtrf_batched_device(p, n, k, ld, B).abs().sum().item()) == 0
+    got = a.cpu().numpy().reshape(B, n, k + 1)
+    ref = p.cpu().numpy().reshape(B, n, ld)[:, :, :k + 1]
+    assert np.array_equal(got, ref)
