@@ -1266,7 +1266,7 @@ struct CtaBand {
   //   warp 0 (chain):      x_b = t_b - G_b^T x_{b+1}
   //   warp 1 (inverter):   rows of M_{b-2} (lanes 0-15) and of G_{b-2} (lanes 16-31): one
   //                        back substitution z^T L_bb = [e_j | row j of B], same instructions
-  //   warps 2-7 (far):     c_{b-1} (row-parallel partial sums, fixed-order reduction), t_{b-1}
+  //   warps 2-7 (far):     c_{b-1} (tensor-path partial sums, fixed-order reduction)
   // and one CTA barrier.  L blocks (and the y entries) stream in with bulk copies nbuf-1
   // blocks ahead of their first use (the inverter's), one mbarrier per ring buffer.
   __device__ void backward() {
@@ -1306,13 +1306,12 @@ struct CtaBand {
         if (threadIdx.x == 0) mbar_expect_tx(bars + 1 + k, 0);
       }
     };
-    // scratch in P (and the D buffers after it): 3 slots of (M_b, G_b), far partials, c, t
+    // scratch in P (and the D buffers after it): 3 slots of (M_b, G_b), far partials, c
     constexpr int kMG = 2 * NB * kLDD;
     constexpr int kFarThreads = kCtaThreads - 64, kFarChunks = kFarThreads / NB;
     double* mg = P;
     double* part = P + 3 * kMG;
-    double* cb = part + kFarThreads;  // c of the block in flight (NB)
-    double* tbuf = cb + NB;           // t of two blocks (2 x NB)
+    double* tbuf = part + kFarThreads + NB;  // c of two blocks (2 x NB), for the chain's M_b^T c_b
     double* dsc = tbuf + 2 * NB;      // the inverter's pivot reciprocals (NB)
     auto mslot = [&](int b) { return mg + (b % 3) * kMG; };
     // inverter: lane j < 16 solves z^T L_bb = e_j^T (row j of M_b), lane 16 + j solves
@@ -1366,29 +1365,26 @@ struct CtaBand {
         double sum = 0.0;
 #pragma unroll
         for (int w = 0; w < kFarThreads / 32; ++w) sum += part[w * NB + i];
-        if (t < NB) cb[t] = t < nb ? yb[k * NB + t] - sum : 0.0;
-        __syncwarp();
-      }
-      if (t < 32) {
-        const int i = t & 15, h = t >> 4;
-        const double* m = mslot(b) + (8 * h) * kLDD + i;  // M(8h + jj, i)
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int jj = 0; jj < 8; jj += 2) {
-          a0 = fma(m[jj * kLDD], cb[8 * h + jj], a0);
-          a1 = fma(m[(jj + 1) * kLDD], cb[8 * h + jj + 1], a1);
-        }
-        double tv = a0 + a1;
-        tv += __shfl_xor_sync(kFull, tv, 16);
-        if (h == 0) tbuf[(b & 1) * NB + i] = tv;
+        // c_b for the chain (which applies M_b^T itself, in parallel with its G_b^T product)
+        if (t < NB) tbuf[(b & 1) * NB + t] = t < nb ? yb[k * NB + t] - sum : 0.0;
       }
     };
-    // chain: x_b = t_b - G_b^T x_{b+1} (lane (i, h): half h of column i of G), to the x ring
-    // and to rhs
+    // chain: x_b = M_b^T c_b - G_b^T x_{b+1} (lane (i, h): half h of columns i of M and G, the
+    // two products in parallel), to the x ring and to rhs
     auto chain = [&](int b, int xb) {  // xb = ring slot of row b*NB
       const int c0 = b * NB, nb = min(NB, n - c0);
       const int i = lane & 15, h = lane >> 4;
-      double a0 = 0.0, a1 = 0.0;
+      double a0 = 0.0, a1 = 0.0, m0 = 0.0, m1 = 0.0;
+      {
+        // t_b = M_b^T c_b (c_b from the far warps), half h of column i of M
+        const double* M = mslot(b) + (8 * h) * kLDD + i;  // M(8h + jj, i)
+        const double* cv = tbuf + (b & 1) * NB + 8 * h;
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += 2) {
+          m0 = fma(M[jj * kLDD], cv[jj], m0);
+          m1 = fma(M[(jj + 1) * kLDD], cv[jj + 1], m1);
+        }
+      }
       if (b + 1 < nblk) {
         const double* G = mslot(b) + NB * kLDD + (8 * h) * kLDD + i;  // G(8h + jj, i)
         int sx = xb + nb + 8 * h;  // row c0 + nb + 8h
@@ -1404,9 +1400,9 @@ struct CtaBand {
           a1 = fma(G[(jj + 1) * kLDD], x1, a1);
         }
       }
-      double s = a0 + a1;
+      double s = (m0 + m1) - (a0 + a1);
       s += __shfl_xor_sync(kFull, s, 16);
-      const double x = tbuf[(b & 1) * NB + i] - s;
+      const double x = s;
       if (lane < nb) {
         int sr = xb + lane;
         if (sr >= g.nx) sr -= g.nx;
