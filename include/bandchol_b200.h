@@ -36,10 +36,10 @@ int bcg_version(void);
 const char* bcg_last_error(void);
 
 /* Workspace bytes bcg_dpbtrf needs for an (n, kd) matrix (0 when the single
- * matrix runs in one CTA).  Holds the per-tile ready flags and the published
- * panel tiles of the multi-CTA kernel.  The caller owns it (no allocation on
- * the hot path); it must be zero-filled before the first use and is left
- * zero-filled by every call that returns 0. */
+ * matrix runs in one CTA).  Holds the per-tile ready flags of the multi-CTA kernel.
+ * The caller owns it (no allocation on the hot path); its contents on entry are
+ * ignored: every launch clears it in stream order, so one workspace may serve calls
+ * that are ordered on one stream, but concurrent calls need distinct workspaces. */
 size_t bcg_dpbtrf_workspace_size(int64_t n, int64_t kd, int64_t ldab);
 
 /* In-place lower band Cholesky A = L L^T of ONE matrix, using the whole GPU.
@@ -49,16 +49,24 @@ size_t bcg_dpbtrf_workspace_size(int64_t n, int64_t kd, int64_t ldab);
 int bcg_dpbtrf(int64_t n, int64_t kd, double* ab, int64_t ldab, int32_t* info,
                void* workspace, size_t workspace_bytes, void* stream);
 
+/* Workspace bytes bcg_dpbtrf_batched / bcg_dpbsv_batched need: 0 when every matrix is
+ * factored by one CTA (its band window fits in shared memory), else the whole-GPU
+ * kernel's flags, reused matrix after matrix (same contract as above). */
+size_t bcg_dpbtrf_batched_workspace_size(int64_t n, int64_t kd, int64_t ldab, int64_t batch);
+
 /* In-place factorization of `batch` independent matrices of the same (n, kd,
  * ldab) stored stride_ab doubles apart; info: device int32[batch].  Each matrix
  * follows the same contract as one bcg_dpbtrf call (the batched interior-point
  * use case of BASELINE.json config C5). */
 int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab,
-                       int64_t batch, int32_t* info, void* stream);
+                       int64_t batch, int32_t* info, void* workspace, size_t workspace_bytes,
+                       void* stream);
 
-/* Solve L L^T x = b in place (b -> x) with the factor from bcg_dpbtrf; nrhs
- * right-hand sides stored ldb doubles apart.  Replaces solve_with_factor
- * (pkg/src/bandchol/core.py:216-240).  info: device int32[1]. */
+/* Solve L L^T X = B in place (B -> X) with the factor from bcg_dpbtrf; nrhs
+ * right-hand sides stored ldb doubles apart, all served by one pass over L per
+ * group of up to 16.  Replaces solve_with_factor (pkg/src/bandchol/core.py:216-240).
+ * info: device int32[1]; a diagonal entry <= 0 gives info = its column + 1 and B
+ * untouched (SingularFactor, core.py:227-230). */
 int bcg_dpbtrs(int64_t n, int64_t kd, const double* ab, int64_t ldab, double* b, int64_t ldb,
                int64_t nrhs, int32_t* info, void* stream);
 
@@ -67,14 +75,21 @@ int bcg_dpbtrs(int64_t n, int64_t kd, const double* ab, int64_t ldab, double* b,
 int bcg_dpbtrs_batched(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab,
                        double* b, int64_t stride_b, int64_t batch, int32_t* info, void* stream);
 
-/* Batched factor + solve (config C5): on return ab holds L and b holds x.  Stream-ordered on
- * `stream`; for kd >= 32 it launches the pipelined factorization and then the streamed
- * two-sweep solve (which skips failed matrices), for narrower bands one fused kernel.
- * info: device int32[batch] with the dpbtrf convention; when a matrix fails its ab and b
- * contents are unspecified (as after a failed reference factorization, which leaves the
- * matrix partially overwritten). */
+/* Batched multi-right-hand-side solve: matrix i has nrhs right-hand sides, column r at
+ * b + i*stride_b + r*ldb (the repeated solves of an interior-point iteration).  One pass
+ * over each L serves up to 16 right-hand sides. */
+int bcg_dpbtrs_batched_nrhs(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab,
+                            double* b, int64_t ldb, int64_t stride_b, int64_t nrhs, int64_t batch,
+                            int32_t* info, void* stream);
+
+/* Batched factor + solve (config C5): on return ab holds L and b holds x.  Stream-ordered
+ * on `stream`: the batched factorization, then the streamed solve of the matrices that
+ * factored.  info: device int32[batch] with the dpbtrf convention; a matrix that fails
+ * keeps its b untouched (LAPACK dpbsv) and its ab partially overwritten (as after a
+ * failed reference factorization).  workspace as for bcg_dpbtrf_batched. */
 int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab,
-                      double* b, int64_t stride_b, int64_t batch, int32_t* info, void* stream);
+                      double* b, int64_t stride_b, int64_t batch, int32_t* info,
+                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* Diagnostics: per-step phase timestamps of the whole-GPU factorization, the
  * analogue of the reference's per-task trace (pkg/src/bandchol/parallel.py:54-62).
@@ -93,6 +108,15 @@ int bcg_set_trace(void* device_buffer, size_t bytes);
 size_t bcg_band_residual_workspace_size(void);
 int bcg_band_residual(int64_t n, int64_t kd, const double* a, int64_t lda, const double* l, int64_t ldl,
                       double* result, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Batched backward error: result[i] (device double[batch]) = the residual of matrix i,
+ * a + i*stride_a against l + i*stride_l (the all-members parity gate of config C5).
+ * Deterministic; workspace >= bcg_band_residual_batched_workspace_size(batch) bytes;
+ * batch <= 65535.  Asynchronous on stream. */
+size_t bcg_band_residual_batched_workspace_size(int64_t batch);
+int bcg_band_residual_batched(int64_t n, int64_t kd, const double* a, int64_t lda, int64_t stride_a,
+                              const double* l, int64_t ldl, int64_t stride_l, int64_t batch,
+                              double* result, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Measurement utility (bench.py): FP64 FMA-pipe peak of the current device in
  * TFLOP/s, from a register-only DFMA loop over every SM (synchronous, ~10 ms).

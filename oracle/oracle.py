@@ -8,6 +8,9 @@ it and has no CPU fallback.
 * `factor_reference`  -- bit-exact restatement of pkg/src/bandchol/reference.py:32-63
                          (C, exactly rounded sums; band_oracle.c).
 * `factor_plain`      -- same recurrence, ordinary rounding, fast (large configs).
+* `factor_plain_batched` -- factor_plain over a batch, one matrix per host thread.
+* `factor_blocked_dense` -- numpy/scipy blocked restatement (blocked.py:259-284 algebra)
+                         for C3/C4 full-L parity in seconds.
 * `solve`             -- pkg/src/bandchol/core.py:216-240.
 * `residual_norm`     -- pkg/src/bandchol/core.py:186-213 (numpy restatement, same ops);
                          `residual_fast` is the C version for the large configs.
@@ -91,6 +94,79 @@ def factor_plain(n: int, kd: int, ldab: int, data: np.ndarray) -> np.ndarray:
     r = lib().bco_factor_plain(n, kd, ldab, _ptr(data))
     if r >= 0:
         raise OracleFailure("NotPositiveDefinite", r)
+    return data
+
+
+def factor_plain_batched(n: int, kd: int, ldab: int, data: np.ndarray, threads: int | None = None) -> np.ndarray:
+    """factor_plain on every row of `data` (batch, >= ldab*n), in place, one matrix per host
+    thread (ctypes drops the GIL).  Returns the per-matrix failing column, -1 = success."""
+    from concurrent.futures import ThreadPoolExecutor
+    assert data.ndim == 2 and data.shape[1] >= ldab * n and data.flags.c_contiguous
+    L = lib()
+    rows = [data[b] for b in range(data.shape[0])]
+    workers = threads or max(1, min(32, os.cpu_count() or 1))
+    with ThreadPoolExecutor(workers) as ex:
+        res = list(ex.map(lambda row: L.bco_factor_plain(n, kd, ldab, _ptr(row)), rows))
+    return np.asarray(res, dtype=np.int64)
+
+
+def factor_blocked_dense(n: int, kd: int, ldab: int, data: np.ndarray, nb: int = 256) -> np.ndarray:
+    """Right-looking blocked band Cholesky in numpy/scipy (multithreaded BLAS), in place --
+    an independent fast checker for the wide configs (C3, C4), where the C loops take
+    minutes.  A dense (kd+nb)-square window slides down the band: POTRF of its leading
+    nb x nb block, TRSM of the rows below, SYRK/GEMM of the trailing window, exactly the
+    tile algebra of blocked.py:259-284 at tile size nb.  Entries outside the band stay
+    exact zeros (they only ever meet zero products).  Raises OracleFailure at the first
+    non-positive pivot (column found by an unblocked pass over the failing block)."""
+    import scipy.linalg as sla
+
+    band = data.reshape(n, ldab)  # band[j, d] = A(j+d, j)
+    w = kd + nb
+
+    def load(win, j0, r_lo, r_hi):
+        # entries (i, j), j0 <= j <= i, r_lo <= i < r_hi, of the untouched band into the
+        # window whose (0, 0) is global (j0, j0)
+        for j in range(j0, min(n, r_hi)):
+            lo, hi = max(r_lo, j), min(r_hi, n, j + kd + 1)
+            if hi > lo:
+                win[lo - j0: hi - j0, j - j0] = band[j, lo - j: hi - j]
+
+    win = np.zeros((w, w))
+    load(win, 0, 0, w)
+    j0 = 0
+    while j0 < n:
+        b = min(nb, n - j0)
+        rows = min(w, n - j0)          # live rows/cols of the window
+        a11 = np.tril(win[:b, :b])
+        try:
+            l11 = np.linalg.cholesky(a11 + np.tril(a11, -1).T)
+            ok = bool(np.all(np.diag(l11) > 0))
+        except np.linalg.LinAlgError:
+            ok = False
+        if not ok:
+            # locate the failing column like reference.py:56-57 (`pivot > 0`, NaN fails)
+            t = a11.copy()
+            for c in range(b):
+                p = t[c, c]
+                if not (p > 0.0):
+                    raise OracleFailure("NotPositiveDefinite", j0 + c)
+                t[c, c] = np.sqrt(p)
+                t[c + 1:, c] /= t[c, c]
+                t[c + 1:, c + 1:] -= np.tril(np.outer(t[c + 1:, c], t[c + 1:, c]))
+            raise OracleFailure("NotPositiveDefinite", j0 + b - 1)
+        win[:b, :b] = l11
+        if rows > b:
+            l21 = sla.solve_triangular(l11, win[b:rows, :b].T, lower=True).T
+            win[b:rows, :b] = l21
+            win[b:rows, b:rows] -= l21 @ l21.T
+        for j in range(j0, j0 + b):  # the finished columns back to the band
+            m = min(kd, n - 1 - j)
+            band[j, : m + 1] = win[j - j0: j - j0 + m + 1, j - j0]
+        nxt = np.zeros((w, w))
+        nxt[: w - b, : w - b] = np.tril(win[b:, b:])
+        win = nxt
+        load(win, j0 + b, j0 + w, j0 + b + w)
+        j0 += b
     return data
 
 

@@ -12,8 +12,8 @@ from .core import BandedMatrix, index_map
 from .engine import (BatchedBandSolver, TraceEvent, pinned_empty, dpbsv_batched_device, dpbtrf_batched_device, dpbtrf_device,
                      dpbtrs_batched_device, dpbtrs_device, factor_batched,
                      factor_blocked_parallel, factor_blocked_serial, factor_solve_batched,
-                     library_version, solve_batched, solve_with_factor)
-from .engine import band_residual_device, residual_norm
+                     library_version, solve_batched, solve_many, solve_with_factor)
+from .engine import band_residual_batched_device, band_residual_device, residual_norm
 from .fixtures import load_matrix, load_matrix_device, save_matrix
 from .errors import (BandCholError, BandwidthNotDivisible, CountOverflow, DeviceError,
                      GridTooSmall, InvalidBandwidth, NotPositiveDefinite, OutOfBand,
@@ -27,9 +27,9 @@ __all__ = [
     "BandedMatrix", "index_map", "TraceEvent", "BatchedBandSolver", "pinned_empty", "dpbsv_batched_device", "dpbtrf_batched_device",
     "dpbtrf_device", "dpbtrs_batched_device", "dpbtrs_device", "factor_batched",
     "factor_blocked_parallel", "factor_blocked_serial", "factor_solve_batched", "library_version",
-    "solve_batched", "solve_with_factor", "BandCholError", "BandwidthNotDivisible", "CountOverflow",
+    "solve_batched", "solve_many", "solve_with_factor", "BandCholError", "BandwidthNotDivisible", "CountOverflow",
     "DeviceError", "GridTooSmall", "InvalidBandwidth", "NotPositiveDefinite", "OutOfBand",
     "ShapeMismatch", "SingularFactor", "flops_approx", "flops_exact", "flops_model", "CONFIGS",
     "BandConfig", "generate_spd", "generate_spd_wide", "make_rhs",
-    "band_residual_device", "residual_norm", "load_matrix", "load_matrix_device", "save_matrix",
+    "band_residual_device", "band_residual_batched_device", "residual_norm", "load_matrix", "load_matrix_device", "save_matrix",
 ]

@@ -22,14 +22,20 @@ SIGNATURES = {
     "bcg_last_error": (ctypes.c_char_p, []),
     "bcg_dpbtrf_workspace_size": (_sz, [_i64, _i64, _i64]),
     "bcg_dpbtrf": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i32p, _vp, _sz, _vp]),
-    "bcg_dpbtrf_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _i64, _i32p, _vp]),
+    "bcg_dpbtrf_batched_workspace_size": (_sz, [_i64, _i64, _i64, _i64]),
+    "bcg_dpbtrf_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _i64, _i32p, _vp, _sz, _vp]),
     "bcg_dpbtrs": (ctypes.c_int, [_i64, _i64, _dp, _i64, _dp, _i64, _i64, _i32p, _vp]),
     "bcg_dpbtrs_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _vp]),
-    "bcg_dpbsv_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _vp]),
+    "bcg_dpbtrs_batched_nrhs": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i64, _i64, _i32p,
+                                               _vp]),
+    "bcg_dpbsv_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _vp, _sz, _vp]),
     "bcg_probe_fp64_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
     "bcg_set_trace": (ctypes.c_int, [_vp, _sz]),
     "bcg_band_residual_workspace_size": (_sz, []),
     "bcg_band_residual": (ctypes.c_int, [_i64, _i64, _dp, _i64, _dp, _i64, _dp, _vp, _sz, _vp]),
+    "bcg_band_residual_batched_workspace_size": (_sz, [_i64]),
+    "bcg_band_residual_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i64, _dp, _vp,
+                                                 _sz, _vp]),
 }
 
 _lib = None

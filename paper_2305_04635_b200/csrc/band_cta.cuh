@@ -1,4 +1,4 @@
-// band_cta.cuh -- one thread block factors (and optionally solves) one band matrix.
+// band_cta.cuh -- one thread block factors one band matrix.
 //
 // Right-looking blocked band Cholesky (the reference's sliding window of
 // blocked.py:1-7, :297-315, re-derived for one CTA).  Step k owns columns
@@ -16,16 +16,13 @@
 //   * POTRF runs in warp 0 with the pivot chain computed REDUNDANTLY in every
 //     lane (p_{c+1} = A'(c+1,c+1) - (A'(c+1,c) rsqrt(p_c))^2 from two values
 //     broadcast one step ahead), so one column costs rsqrt + mul + fma on the
-//     critical path instead of rsqrt + shuffle + mul + fma.  The forward sweep of
-//     the solve rides along in the same loop.
+//     critical path instead of rsqrt + shuffle + mul + fma.
 //   * Lookahead: the update of step k is split; the part that touches the next
 //     panel's columns runs first, then warp 0 factors the next diagonal block
 //     while warps 1-7 finish the rest of step k's update.
 //   * The trailing update runs on the FP64 tensor path (mma.sync m8n8k4 f64 ->
 //     DMMA), 16x16 warp tiles, operands from a dense panel copy P whose leading
 //     dimension is 4 (mod 16) doubles (conflict-free fragment loads).
-//   * Backward sweep (fused solve): L is streamed back through the same ring with a
-//     cp.async pipeline several blocks deep.
 #pragma once
 #include <type_traits>
 #include <cstdint>
@@ -44,6 +41,17 @@ constexpr int kCopyThread = kCtaThreads - 32;
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// 8-byte cp.async; ok = false writes zeros (src-size 0, src not read)
+__device__ __forceinline__ void cp_async8_zfill(double* smem, const double* gmem, bool ok) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
+}
+// arrive on an mbarrier once every prior cp.async of this thread has landed (counted
+// against the barrier's expected arrivals)
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
@@ -183,32 +191,18 @@ struct CtaGeom {
   int n, kd, ldab;  // matrix geometry
   int lds, nslot;   // shared window: nslot column slots of lds doubles
   int pld;          // leading dimension of the dense panel P (>= kd rounded up to 16, = 4 mod 16)
-  int nx;           // ring of rhs / solution entries (bw): nx slots (= nslot in the fused kernel)
 };
 
-// The panel buffer P; the backward sweep reuses it for two L11^-1 blocks.
-__host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom& g, bool solve) {
-  // backward sweep scratch: 3 x (M_b, G_b) + far partials + c + 2 t, of which the two D
-  // buffers that follow P in shared memory hold 2 * nb_block * (nb_block + 4) doubles
-  const size_t p = (size_t)nb_block * g.pld;
-  const size_t need = 6 * (size_t)nb_block * (nb_block + 4) + 192 + 4 * (size_t)nb_block;
-  const size_t inv = need - 2 * (size_t)nb_block * (nb_block + 4);
-  return (solve && inv > p) ? inv : p;
-}
-
-// Column-block buffers of the streamed sweeps (at most 7, at least 5: host geometry).
-template <class G>
-__host__ __device__ inline int cta_sweep_buffers(int nb_block, const G& g) {
-  const int n = g.nslot / nb_block;
-  return n < 7 ? n : 7;
+// The dense panel buffer P (nb_block x pld).
+__host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom& g) {
+  return (size_t)nb_block * g.pld;
 }
 
 // Shared-memory footprint (bytes) of one CTA for block size NB.
-__host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g, bool solve) {
+__host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g) {
   // D: two L11 / L11^-1 buffers (the pipelined factorization alternates them by step)
-  size_t d = (size_t)g.nslot * g.lds + cta_panel_doubles(nb_block, g, solve) + 2 * (size_t)nb_block * (nb_block + 4) +
+  size_t d = (size_t)g.nslot * g.lds + cta_panel_doubles(nb_block, g) + 2 * (size_t)nb_block * (nb_block + 4) +
              nb_block;
-  if (solve) d += (size_t)g.nx + (size_t)cta_sweep_buffers(nb_block, g) * nb_block;  // rhs ring + staged y
   return d * sizeof(double) + 64;
 }
 
@@ -216,42 +210,36 @@ __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g,
 // kd + 1, the ring and panel strides exactly as make_geom() (bandchol_b200.cu) picks them,
 // so index arithmetic folds to constants and frees registers in the hot loops; n stays
 // runtime.  KD = 0 selects the runtime CtaGeom.
-template <int KD, bool kSolve>
+template <int KD>
 struct GeomFixed {
   int n;
   static constexpr int kd = KD, ldab = KD + 1, lds = KD + 1;
-  static constexpr int ns0 = (kSolve && KD + 16 < 5 * 16) ? 5 * 16 : KD + 16;
-  static constexpr int nslot = (ns0 & 1) ? ns0 + 1 : ns0, nx = nslot;
+  static constexpr int ns0 = KD + 16;
+  static constexpr int nslot = (ns0 & 1) ? ns0 + 1 : ns0;
   static constexpr int pld = KD + ((4 - KD % 16) + 16) % 16;
   __host__ __device__ GeomFixed(const CtaGeom& x) : n(x.n) {}
   // true when the runtime geometry the host chose is exactly this one
   __host__ __device__ static bool matches(const CtaGeom& x) {
-    return x.kd == kd && x.ldab == ldab && x.lds == lds && x.nslot == nslot && x.nx == nx && x.pld == pld;
+    return x.kd == kd && x.ldab == ldab && x.lds == lds && x.nslot == nslot && x.pld == pld;
   }
 };
-template <int KD, bool kSolve>
-struct GeomOf { using type = GeomFixed<KD, kSolve>; };
-template <bool kSolve>
-struct GeomOf<0, kSolve> { using type = CtaGeom; };
+template <int KD>
+struct GeomOf { using type = GeomFixed<KD>; };
+template <>
+struct GeomOf<0> { using type = CtaGeom; };
 
-template <int NB, bool kSolve, int KD = 0>
+template <int NB, int KD = 0>
 struct CtaBand {
   static_assert(NB == 16, "block size: lanes 16-31 of the POTRF warp invert L11");
-  const typename GeomOf<KD, kSolve>::type g;
+  const typename GeomOf<KD>::type g;
   double* __restrict__ ab;   // this matrix in global memory
-  double* __restrict__ rhs;  // its right-hand side (kSolve)
   double* win;               // shared ring of column slots
   double* P;                 // NB x pld dense panel, P[c*pld + r] = L(j0+nb+r, j0+c)
   static constexpr int kLDD = NB + 4;  // D stride (= 4 mod 16: conflict-free DMMA fragments)
   double* D;                 // L11, D[c*kLDD + r] = L(r, c); then L11^-1, D[i*kLDD + j] = Linv(i, j)
-  double* Dinv;              // 3 x NB doubles of sweep scratch (aliases the second D buffer,
-                             // free outside the factorization)
   double* lbuf;              // NB doubles: sink for the inverse lanes' column stores
-  double* bw;                // ring of rhs / solution entries, slot(i) like columns
-  double* yb;                // backward sweep: nbuf x NB staged y entries; factor: y of the last two blocks
-  unsigned long long* bars;  // mbarriers: [0] window loads, [1 + k] backward buffer k
+  unsigned long long* bars;  // mbarrier [0]: window loads
   unsigned long long* sig;   // pipelined factorization: [0] panel ready, [1] column 0 updated, [2 + (k&1)] update done
-  unsigned* bphase;          // smem: parity of the next wait on bars[1 + k]
   unsigned phase = 0;        // parity of the next wait on bars[0] (uniform register)
   bool pending = false;      // a load_cols is in flight
   bool fast = false;         // every column chunk meets the bulk-copy alignment rules
@@ -348,7 +336,7 @@ struct CtaBand {
     if (fast && g.ldab % 2 == 1) fast = ((g.n - min(g.n, g.kd + NB)) % 2 == 0) && (min(g.n, g.kd + NB) % 2 == 0);
   }
 
-  // async load of columns [jlo, jhi) (and their rhs entries); complete with wait_cols()
+  // async load of columns [jlo, jhi); complete with wait_cols()
   // sj: ring slot of column jlo when the caller knows it (saves a division), else -1
   __device__ void load_cols(int jlo, int jhi, int sj = -1) {
     if (sj < 0) sj = jlo % g.nslot;
@@ -361,14 +349,6 @@ struct CtaBand {
         const int c1 = min(jhi - jlo, g.nslot - s0);
         bulk_g2s(win + (size_t)s0 * g.lds, ab + (int64_t)jlo * g.ldab, c1 * col, bars);
         if (c1 < jhi - jlo) bulk_g2s(win, ab + (int64_t)(jlo + c1) * g.ldab, (jhi - jlo - c1) * col, bars);
-      }
-      if (kSolve) {
-        for (int j = jlo + threadIdx.x; j < jhi; j += kCtaThreads) {
-          int sl = sj + (j - jlo);
-          if (sl >= g.nslot) sl -= g.nslot;
-          cp_async8(bw + sl, rhs + j);
-        }
-        cp_async_commit();
       }
       pending = true;
       return;
@@ -395,14 +375,12 @@ struct CtaBand {
                    (unsigned)bc * g.ldab * sizeof(double), bars);
       }
     }
-    if (kSolve)
-      for (int j = jlo + threadIdx.x; j < jhi; j += kCtaThreads) cp_async8(bw + (j % g.nslot), rhs + j);
     cp_async_commit();
     pending = true;
   }
   // all threads: the last load_cols has landed and is visible
   __device__ __forceinline__ void wait_cols() {
-    if (kSolve || !fast) cp_async_wait_all();
+    if (!fast) cp_async_wait_all();
     mbar_wait(bars, phase);
     phase ^= 1u;
     pending = false;
@@ -437,7 +415,7 @@ struct CtaBand {
     if (threadIdx.x == kCopyThread) bulk_commit();
   }
 
-  // Warp pw: Cholesky of the nb x nb diagonal block at column j0 (+ forward sweep).
+  // Warp pw: Cholesky of the nb x nb diagonal block at column j0.
   // Lane r holds row r.  Returns the local failing column or -1 (uniform).
   //
   // Straight-line for every block: a short last block (nb < NB) is padded with identity
@@ -446,7 +424,6 @@ struct CtaBand {
   // column suffices), lanes NB..31 build L11^-1 along the way, and failure is found
   // once at the end: after a non-positive / NaN pivot every later pivot of the block is
   // NaN, so the first failing column is the first lane whose L(r, r) is not > 0.
-  template <bool kFwd>
   __device__ int potrf_diag(int s0, int j0, int nb) {
     const int r = threadIdx.x & 31;
     double row[NB];
@@ -474,8 +451,6 @@ struct CtaBand {
         row[c] = in ? v : ((inv ? c == r - NB : (r >= nb && c == r)) ? e : 0.0);
       }
     }
-    double s = 0.0;
-    if (kFwd && r < nb) s = bw[slot_from(s0, j0, j0 + r)];
     // chain state, identical in every lane: p = pivot of column c, (alpha, beta) =
     // (A'(c+1,c), A'(c+1,c+1)) through column c-1, broadcast by lane c+1 a step early.
     double p = __shfl_sync(kFull, row[0], 0);
@@ -501,10 +476,6 @@ struct CtaBand {
         const double bn = fma(-lrc, lrc, row[c + 2 < NB ? c + 2 : 0]);
         alpha_n = shfl_early(row[c + 1 < NB ? c + 1 : 0], c + 2);
         beta_n = shfl_early(bn, c + 2);
-      }
-      if (kFwd) {
-        const double yc = __shfl_sync(kFull, s, c) * rs;
-        s = (r == c) ? yc : ((r > c) ? fma(-lrc, yc, s) : s);
       }
       row[c] = lrc;
       double* dc = D + c * kLDD;  // column c of L11 (rows < c: don't-care)
@@ -533,11 +504,6 @@ struct CtaBand {
     for (int c = 0; c < NB; ++c) {
       const int sl = c < sw ? s0 + c : s0 + c - g.nslot;
       if (c <= r && r < nb && r - c <= g.kd) win[sl * g.lds + (r - c)] = row[c];
-    }
-    if (kFwd && r < nb) {
-      bw[slot_from(s0, j0, j0 + r)] = s;
-      rhs[j0 + r] = s;
-      yb[((j0 / NB) & 1) * NB + r] = s;  // y of this block for update_rhs (ring slot is reused)
     }
     // D <- L11^-1, row-major (D[i*kLDD + j] = Linv(i, j)), once every lane is done
     // reading L11 from it
@@ -696,20 +662,6 @@ struct CtaBand {
     }
   }
 
-  // Forward-sweep update of the trailing rhs entries: b_i -= sum_c P(i,c) y_c.
-  // Rows [lo, min(hi, m)) by threads tid, tid + nt, ...
-  __device__ void update_rhs(int s0, int j0, int nb, int m, int lo, int hi, int tid, int nt) {
-    const int base = j0 + nb;
-    hi = min(hi, m);
-    for (int i = lo + tid; i < hi; i += nt) {
-      double s = 0.0;
-#pragma unroll
-      for (int c = 0; c < NB; ++c)
-        if (c < nb) s = fma(P[c * g.pld + i], yb[((j0 / NB) & 1) * NB + c], s);
-      bw[slot_from(s0, j0, base + i)] -= s;
-    }
-  }
-
   // ---- pipelined factorization (kd >= 32) -------------------------------------------
   // Three warp roles, no CTA-wide barrier inside the column loop:
   //   pivot (SMSP 0): SYRK of tile (0,0) of update(k-1) -> POTRF(k) (+ L11^-1) -> TRSM of
@@ -777,13 +729,13 @@ struct CtaBand {
       if (k >= 2) mbar_wait(sig + 2 + (k & 1), ((k - 2) >> 1) & 1);  // update(k-2) complete
       trace_stamp(k, 1);
       if (k >= 1) {
-        // tile (0,0) of update(k-1) (this block) and its rhs rows, from P rows 0..15 = X0(k-1)
+        // tile (0,0) of update(k-1) (this block), from P rows 0..15 = X0(k-1)
         update_tiles(sp, j0 - NB, NB, mp, 0, 1, 0, 1);
         __syncwarp();
       }
       trace_stamp(k, 2);
       D = Dbase + (k & 1) * NB * kLDD;
-      const int f = potrf_diag<false>(s0, j0, nb);
+      const int f = potrf_diag(s0, j0, nb);
       trace_stamp(k, 3);
       // column 0 of update(k-1) done: A(k+1, k) is final and P rows 0..15 are free.  Also
       // waited when there is no TRSM (last block, failure): it proves every worker and the
@@ -916,12 +868,10 @@ struct CtaBand {
     return fail < 0 ? -1 : fail;
   }
 
-  // Whole factorization (+ forward sweep when kSolve, lock-step loop only).  Returns -1 or
-  // the failing column.
+  // Whole factorization: the pipelined kernel for kd >= 32, else the lock-step loop below.
+  // Returns -1 or the failing column.
   __device__ int factor() {
-    // (the fused solve runs the lock-step loop below: for kd >= 32 bcg_dpbsv_batched factors with
-    // the pipelined kernel and then runs the streamed solve, which measured faster)
-    if (!kSolve && g.kd >= 32) return factor_la();
+    if (g.kd >= 32) return factor_la();
     const int n = g.n, kd = g.kd;
     __shared__ int s_fail;
     const int warp = threadIdx.x >> 5;
@@ -947,21 +897,19 @@ struct CtaBand {
       // shuffles compile to plain SHFL instead of collective divergence handling
       const int wu = warp_uniform(warp);
       if (wu == pw) {
-        // the previous step's update of this block (tile (0,0)) and of its rhs rows,
-        // then POTRF: no CTA barrier between the TRSM that fed them and this POTRF
+        // the previous step's update of this block (tile (0,0)), then POTRF: no CTA
+        // barrier between the TRSM that fed it and this POTRF
         if (jp >= 0) {
           update_tiles(sp, jp, nbp, mp, 0, 1, 0, 1);
-          if (kSolve) update_rhs(sp, jp, nbp, mp, 0, NB, threadIdx.x & 31, 32);
           __syncwarp();
         }
         trace_stamp(step, 3);
-        const int f = potrf_diag<kSolve>(s0, j0, nb);
+        const int f = potrf_diag(s0, j0, nb);
         if ((threadIdx.x & 31) == 0) s_fail = f;
         trace_stamp(step, 4);
       } else if (wk >= 0 && jp >= 0) {
         // the rest of the previous step's update, on the other three SM sub-partitions
         update_tiles(sp, jp, nbp, mp, 1, 1 << 20, wk, kCtaWarps - 2);
-        if (kSolve) update_rhs(sp, jp, nbp, mp, NB, 1 << 20, (threadIdx.x & 31) + 32 * wk, 32 * (kCtaWarps - 2));
         if (wk == 0) trace_stamp(step, 5);
       }
       __syncthreads();
@@ -982,13 +930,11 @@ struct CtaBand {
       if (pending) wait_cols();  // columns prefetched by the previous step
       else __syncthreads();
       if (threadIdx.x < 32) trace_stamp(step, 1);
-      store_cols(j0, nb, kSolve ? s0 : -1);
+      store_cols(j0, nb);
       // prefetch the columns step k+1 brings into the window (into the slots just
       // written back, once the write-back has read them)
       const int jlo = j0 + NB + kd;
-      // (the slot hints measured faster in the fused kernel only; the factor-only kernel
-      // keeps the self-computed slots)
-      if (jlo < n) load_cols(jlo, min(n, jlo + NB), kSolve ? slot_from(s0, j0, jlo) : -1);
+      if (jlo < n) load_cols(jlo, min(n, jlo + NB));
       if (threadIdx.x < 32) trace_stamp(step, 2);
       if (j0 + nb >= n) break;
       jp = j0; sp = s0; nbp = nb; mp = m;
@@ -1006,464 +952,6 @@ struct CtaBand {
     if (threadIdx.x == kCopyThread) {
       bulk_wait0();
       fence_async_global();
-    }
-    __syncthreads();
-  }
-
-  // L11^-1 of a column block held in the ring (blk: NB column slots of lds doubles, nb
-  // valid columns; columns past nb are identity).  Warp-level: lane j forward-substitutes
-  // L11 x = e_j with the reciprocal pivots computed up front (independent: full ILP).
-  // kRowMajor: li[i*kLDD + j] = Linv(i, j); else li[j*kLDD + i] = Linv(i, j).
-  template <bool kWhole, bool kRowMajor>
-  __device__ void invert_l11(const double* blk, int nb, double* li) const {
-    if (kWhole) nb = NB;
-    const int j = threadIdx.x & 31;
-    double dk[NB];
-#pragma unroll
-    for (int kk = 0; kk < NB; ++kk) dk[kk] = (kWhole || kk < nb) ? rcp_nr(blk[kk * g.lds]) : 1.0;
-    double t[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) t[i] = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-    for (int kk = 0; kk < NB; ++kk) {
-      const double* col = blk + kk * g.lds;
-      t[kk] *= dk[kk];
-#pragma unroll
-      for (int i = kk + 1; i < NB; ++i) {
-        if (kWhole) {
-          t[i] = fma(-col[i - kk], t[kk], t[i]);
-        } else {
-          const bool in = i < nb && i - kk <= g.kd;
-          const double lv = col[in ? i - kk : 0];
-          t[i] = fma(in ? -lv : 0.0, t[kk], t[i]);
-        }
-      }
-    }
-    if (j < NB) {
-#pragma unroll
-      for (int i = 0; i < NB; ++i) li[kRowMajor ? i * kLDD + j : j * kLDD + i] = t[i];
-    }
-  }
-  template <bool kRowMajor>
-  __device__ void invert_block(const double* blk, int nb, double* li) const {
-    if (nb == NB && g.kd >= NB - 1) invert_l11<true, kRowMajor>(blk, nb, li);
-    else invert_l11<false, kRowMajor>(blk, nb, li);
-  }
-
-  // Forward sweep L y = b for the standalone solve (rhs holds b, receives y).
-  //
-  // Column blocks stream in through the same buffer ring as the backward sweep (bulk
-  // copies kDepth blocks ahead); bw (nx slots) holds the running right-hand side of the
-  // kd+NB rows in flight.  Iteration b (mirror image of backward()):
-  //   warp 0:     near update of block b by block b-1 (16x16 GEMV), y_b = L11^-1 s_b
-  //   warp 1:     L11^-1 of block b+1
-  //   warps 2-7:  far update of the rows beyond block b by block b-1 (one thread per row),
-  //               then the rhs entries of the rows entering the ring
-  __device__ void forward() {
-    const int n = g.n, kd = g.kd;
-    const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
-    constexpr int kDepth = 4;
-    const int nbuf = cta_sweep_buffers(NB, g);
-    const int nblk = (n + NB - 1) / NB;
-    double* ycur = Dinv;  // y of the last two blocks (2 x NB)
-    const bool early_issue = fast && nbuf >= kDepth + 3;
-    double* li_buf = P;
-    // parity of the next wait on buffer k (bit k) and ring positions, tracked without divisions
-    unsigned pbits = 0;
-    for (int k = 0; k < nbuf; ++k) pbits |= (bphase[k] & 1u) << k;
-    auto wait_buf = [&](int k) {
-      mbar_wait(bars + 1 + k, (pbits >> k) & 1u);
-      pbits ^= 1u << k;
-    };
-    auto inc = [](int v, int by, int mod) { v += by; return v >= mod ? v - mod : v; };
-    auto issue = [&](int b, int k) {  // k = b % nbuf
-      if (b >= nblk) return;
-      const int c0 = b * NB;
-      const int cols = min(NB, n - c0);
-      if (fast) {
-        if (threadIdx.x == 0) {
-          const unsigned bytes = (unsigned)cols * g.ldab * sizeof(double);
-          mbar_expect_tx(bars + 1 + k, bytes);
-          bulk_g2s(win + (size_t)(k * NB) * g.lds, ab + (int64_t)c0 * g.ldab, bytes, bars + 1 + k);
-        }
-      } else {
-        for (int c = 0; c < cols; ++c) {
-          double* sp = win + (size_t)(k * NB + c) * g.lds;
-          const double* gp = ab + (int64_t)(c0 + c) * g.ldab;
-          for (int o = threadIdx.x; o < g.ldab; o += kCtaThreads) sp[o] = gp[o];
-        }
-        if (threadIdx.x == 0) mbar_expect_tx(bars + 1 + k, 0);
-      }
-    };
-    auto invert = [&](int b, int k) {  // warp 1: L11^-1 of block b into li_buf[b & 1]
-      invert_block<true>(win + (size_t)k * NB * g.lds, min(NB, n - b * NB), li_buf + (b & 1) * NB * kLDD);
-    };
-    // bw accumulates the far updates of the rows in flight (zero when a row enters); warp 0
-    // adds the right-hand side itself, prefetched one block ahead into a register
-    for (int i = threadIdx.x; i < min(n, kd + NB); i += kCtaThreads) bw[i % g.nx] = 0.0;
-    double rnext = (warp == 0 && lane < min(NB, n)) ? rhs[lane] : 0.0;
-    for (int d = 0; d < kDepth; ++d) issue(d, d % nbuf);
-    wait_buf(0);
-    __syncthreads();
-    if (warp == 1) invert(0, 0);
-    int kb = 0, xb = 0;  // buffer of block b, ring slot of row b*NB
-    for (int b = 0; b < nblk; ++b) {
-      const int kp1 = inc(kb, 1, nbuf), km1 = kb == 0 ? nbuf - 1 : kb - 1;
-      const int c0 = b * NB;
-      const int nb = min(NB, n - c0);
-      if (threadIdx.x < 32) trace_stamp(b, 0);
-      if (b + 1 < nblk) wait_buf(kp1);
-      __syncthreads();  // L11^-1(b), far(b-1) and the entering rows are in place
-      if (threadIdx.x < 32) trace_stamp(b, 1);
-      if (warp == 0) {
-        const int r = lane;
-        const double rcur = rnext;
-        if (c0 + NB + r < n && r < NB) rnext = rhs[c0 + NB + r];  // next block's b, in flight
-        double v = (r < nb) ? rcur + bw[inc(xb, r, g.nx)] : 0.0;
-        if (b > 0 && r < nb) {
-          // near: rows of block b in the columns of block b-1
-          const double* blk = win + (size_t)km1 * NB * g.lds;
-          const double* yp = ycur + ((b - 1) & 1) * NB;
-          double a0 = 0.0, a1 = 0.0;
-          if (kd >= 2 * NB - 1) {  // every (row of b, column of b-1) pair is in the band
-#pragma unroll
-            for (int c = 0; c < NB; c += 2) {
-              a0 = fma(blk[c * g.lds + NB + r - c], yp[c], a0);
-              a1 = fma(blk[(c + 1) * g.lds + NB + r - c - 1], yp[c + 1], a1);
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < NB; c += 2) {
-              const int o0 = NB + r - c, o1 = o0 - 1;
-              if (o0 <= kd) a0 = fma(blk[c * g.lds + o0], yp[c], a0);
-              if (o1 <= kd) a1 = fma(blk[(c + 1) * g.lds + o1], yp[c + 1], a1);
-            }
-          }
-          v -= a0 + a1;
-        }
-        double* ss = Dinv + 2 * NB;
-        if (r < NB) ss[r] = v;
-        __syncwarp();
-        const double* li = li_buf + (b & 1) * NB * kLDD + (r < NB ? r : 0) * kLDD;
-        double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-        for (int c = 0; c < NB; c += 4) {
-          const double2 l01 = *reinterpret_cast<const double2*>(li + c);
-          const double2 l23 = *reinterpret_cast<const double2*>(li + c + 2);
-          const double2 s01 = *reinterpret_cast<const double2*>(ss + c);
-          const double2 s23 = *reinterpret_cast<const double2*>(ss + c + 2);
-          x0 = fma(l01.x, s01.x, x0);
-          x1 = fma(l01.y, s01.y, x1);
-          x0 = fma(l23.x, s23.x, x0);
-          x1 = fma(l23.y, s23.y, x1);
-        }
-        v = x0 + x1;
-        if (r < nb) {
-          ycur[(b & 1) * NB + r] = v;
-          rhs[c0 + r] = v;
-        }
-        trace_stamp(b, 2);
-        // with >= kDepth + 3 buffers the slot block b + kDepth goes to (block b-3's) is already
-        // free: the chain warp issues it now rather than after the barrier
-        if (early_issue) issue(b + kDepth, inc(kb, kDepth, nbuf));
-      } else if (warp == 1) {
-        if (b + 1 < nblk) invert(b + 1, kp1);
-        trace_stamp(b, 4);
-      } else if (b > 0) {
-        // far: rows i in [c0 + nb, (c0 - NB) + NB - 1 + kd] lose L(i, block b-1) . y_{b-1}
-        const double* blk = win + (size_t)km1 * NB * g.lds;
-        const double* yp = ycur + ((b - 1) & 1) * NB;
-        const int cprev = c0 - NB;
-        const int ihi = min(n - 1, cprev + NB - 1 + kd);
-        for (int i = c0 + nb + (int)threadIdx.x - 64; i <= ihi; i += kCtaThreads - 64) {
-          double acc0 = 0.0, acc1 = 0.0;
-          const int o0 = i - cprev;
-          if (o0 - (NB - 1) <= kd && o0 <= kd) {  // the whole row segment is in the band
-#pragma unroll
-            for (int c = 0; c < NB; c += 2) {
-              acc0 = fma(blk[c * g.lds + o0 - c], yp[c], acc0);
-              acc1 = fma(blk[(c + 1) * g.lds + o0 - c - 1], yp[c + 1], acc1);
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < NB; c += 2) {
-              if (o0 - c <= kd) acc0 = fma(blk[c * g.lds + o0 - c], yp[c], acc0);
-              if (o0 - c - 1 <= kd) acc1 = fma(blk[(c + 1) * g.lds + o0 - c - 1], yp[c + 1], acc1);
-            }
-          }
-          bw[i % g.nx] -= acc0 + acc1;
-        }
-        if (warp == 2) trace_stamp(b, 5);
-      }
-      if (warp >= 2) {
-        // rows entering the ring: first touched by far(b) in the next iteration
-        const int lo = c0 + kd + NB, hi = min(n, lo + NB);
-        for (int i = lo + (int)threadIdx.x - 64; i < hi; i += kCtaThreads - 64) bw[i % g.nx] = 0.0;
-      }
-      __syncthreads();
-      if (threadIdx.x < 32) trace_stamp(b, 3);
-      if (!early_issue) issue(b + kDepth, inc(kb, kDepth, nbuf));  // block b-1's buffer is free now
-      kb = kp1;
-      xb = inc(xb, NB, g.nx);
-    }
-    __syncthreads();
-    if (threadIdx.x < nbuf) {
-      int cnt = 0;
-      for (int b = threadIdx.x; b < nblk; b += nbuf) ++cnt;
-      bphase[threadIdx.x] = (bphase[threadIdx.x] + (unsigned)cnt) & 1u;
-    }
-    if (threadIdx.x == 0) fence_async_global();  // y (generic stores) -> the backward's bulk reads
-    __syncthreads();
-  }
-
-  // Backward-sweep inverter (one warp): lane j < 16 solves z^T L_bb = e_j^T (row j of
-  // M = L_bb^-1), lane 16 + j solves z^T L_bb = row j of B (row j of G = B M, B = L(rows of
-  // the next block, cols of this one)); z_k = r_k / L_kk for k = NB-1..0, then
-  // r_i -= z_k L(k, i) for i < k, L entries broadcast from the ring buffer.  Rows go to
-  // out[j*kLDD] (M) and out[NB*kLDD + j*kLDD] (G).  kWhole: every entry in the band.
-  template <bool kWhole>
-  __device__ void invert_bt(const double* blk, int nb, int c0, double* out, double* dsc) const {
-    const int lane = threadIdx.x & 31, j = lane & 15;
-    const bool isg = lane >= 16;
-    if (lane < NB) dsc[lane] = lane < nb ? rcp_nr(blk[lane * g.lds]) : 1.0;
-    double r[NB];
-#pragma unroll
-    for (int kk = 0; kk < NB; ++kk) {
-      const int o = NB + j - kk;  // B(j, kk) = L(c0 + NB + j, c0 + kk)
-      const bool inb = kWhole || (kk < nb && c0 + NB + j < g.n && o <= g.kd);
-      const double bv = blk[kk * g.lds + (inb ? o : 0)];
-      r[kk] = isg ? (inb ? bv : 0.0) : (kk == j ? 1.0 : 0.0);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int kk = NB - 1; kk >= 0; --kk) {
-      const double z = r[kk] * dsc[kk];
-      r[kk] = z;
-#pragma unroll
-      for (int i = 0; i < kk; ++i) {
-        if (kWhole) {
-          r[i] = fma(-blk[i * g.lds + kk - i], z, r[i]);
-        } else {
-          const bool inb = kk < nb && kk - i <= g.kd;
-          const double lv = blk[i * g.lds + (inb ? kk - i : 0)];
-          r[i] = fma(inb ? -lv : 0.0, z, r[i]);
-        }
-      }
-    }
-    double* dst = out + (isg ? NB * kLDD : 0) + j * kLDD;
-#pragma unroll
-    for (int kk = 0; kk < NB; kk += 2) *reinterpret_cast<double2*>(dst + kk) = make_double2(r[kk], r[kk + 1]);
-    __syncwarp();
-  }
-
-  // Backward sweep L^T x = y (y in rhs after the forward sweep).
-  //
-  // Block b = columns [b*NB, b*NB+nb).  With M_b = L_bb^-1, B_b = L(rows of block b+1, cols
-  // of block b) and G_b = B_b M_b:
-  //   x_b = M_b^T (c_b - B_b^T x_{b+1}) = t_b - G_b^T x_{b+1},
-  //   c_b = y_b - sum over rows beyond block b+1 of L(i, block b)^T x_i,  t_b = M_b^T c_b,
-  // so the per-block chain is one 16x16 product.  Iteration b runs
-  //   warp 0 (chain):      x_b = t_b - G_b^T x_{b+1}
-  //   warp 1 (inverter):   rows of M_{b-2} (lanes 0-15) and of G_{b-2} (lanes 16-31): one
-  //                        back substitution z^T L_bb = [e_j | row j of B], same instructions
-  //   warps 2-7 (far):     c_{b-1} (tensor-path partial sums, fixed-order reduction)
-  // and one CTA barrier.  L blocks (and the y entries) stream in with bulk copies nbuf-1
-  // blocks ahead of their first use (the inverter's), one mbarrier per ring buffer.
-  __device__ void backward() {
-    const int n = g.n;
-    const int lane = threadIdx.x & 31, warp = warp_uniform(threadIdx.x >> 5);
-    const int nbuf = cta_sweep_buffers(NB, g);
-    const int nblk = (n + NB - 1) / NB;
-    const bool bulk_y = fast && !(((uintptr_t)rhs) & 15);
-    // parity of the next wait on buffer k's mbarrier, bit k (no divisions in the loop)
-    unsigned pbits = 0;
-    for (int k = 0; k < nbuf; ++k) pbits |= (bphase[k] & 1u) << k;
-    auto wait_buf = [&](int k) {
-      mbar_wait(bars + 1 + k, (pbits >> k) & 1u);
-      pbits ^= 1u << k;
-    };
-    auto issue = [&](int b, int k) {  // k = b % nbuf
-      if (b < 0) return;
-      const int c0 = b * NB;
-      const int cols = min(NB, n - c0);
-      if (fast) {
-        if (threadIdx.x == 0) {
-          const unsigned bytes = (unsigned)cols * g.ldab * sizeof(double);
-          const unsigned ybytes = (bulk_y && cols % 2 == 0) ? cols * sizeof(double) : 0;
-          mbar_expect_tx(bars + 1 + k, bytes + ybytes);
-          bulk_g2s(win + (size_t)(k * NB) * g.lds, ab + (int64_t)c0 * g.ldab, bytes, bars + 1 + k);
-          if (ybytes) bulk_g2s(yb + k * NB, rhs + c0, ybytes, bars + 1 + k);
-          else for (int t = 0; t < cols; ++t) yb[k * NB + t] = rhs[c0 + t];
-        }
-      } else {
-        // element-wise fallback: synchronous copies, visible after the caller's barrier
-        for (int c = 0; c < cols; ++c) {
-          double* sp = win + (size_t)(k * NB + c) * g.lds;
-          const double* gp = ab + (int64_t)(c0 + c) * g.ldab;
-          for (int o = threadIdx.x; o < g.ldab; o += kCtaThreads) sp[o] = gp[o];
-        }
-        for (int t = threadIdx.x; t < cols; t += kCtaThreads) yb[k * NB + t] = rhs[c0 + t];
-        if (threadIdx.x == 0) mbar_expect_tx(bars + 1 + k, 0);
-      }
-    };
-    // scratch in P (and the D buffers after it): 3 slots of (M_b, G_b), far partials, c
-    constexpr int kMG = 2 * NB * kLDD;
-    constexpr int kFarThreads = kCtaThreads - 64, kFarChunks = kFarThreads / NB;
-    double* mg = P;
-    double* part = P + 3 * kMG;
-    double* tbuf = part + kFarThreads + NB;  // c of two blocks (2 x NB), for the chain's M_b^T c_b
-    double* dsc = tbuf + 2 * NB;      // the inverter's pivot reciprocals (NB)
-    auto mslot = [&](int b) { return mg + (b % 3) * kMG; };
-    // inverter: lane j < 16 solves z^T L_bb = e_j^T (row j of M_b), lane 16 + j solves
-    // z^T L_bb = row j of B_b (row j of G_b = B_b M_b); z_k = r_k / L_kk for k = 15..0, then
-    // r_i -= z_k L(k, i) for i < k (L entries broadcast from the ring buffer)
-    auto invert = [&](int b, int k) {
-      const int c0 = b * NB, nb = min(NB, n - c0);
-      const double* blk = win + (size_t)k * NB * g.lds;
-      if (nb == NB && g.kd >= 2 * NB - 1 && c0 + 2 * NB <= n)
-        invert_bt<true>(blk, nb, c0, mslot(b), dsc);
-      else
-        invert_bt<false>(blk, nb, c0, mslot(b), dsc);
-    };
-    // far warps: c_b = y_b - sum_{rows beyond block b+1} L(i, c0+c) x_i (thread (chunk q,
-    // column c) sums rows o_lo + q, + kFarChunks, ...; chunk partials added in a fixed order),
-    // then t_b = M_b^T c_b by the first far warp (lane (i, h): half h of row i's products)
-    auto far_t = [&](int b, int k, int sx) {  // k = b % nbuf, sx = ring slot of row b*NB + nb + NB
-      // (tensor path: sum_rows L(row, c0 + col) x_row is a 16 x R by R x 1 product, k-steps of
-      // four rows dealt round-robin to the six warps, x in column 0 of B; the six partial
-      // columns are added in a fixed order, so the result is deterministic)
-      const int c0 = b * NB;
-      const int nb = min(NB, n - c0);
-      const double* blk = win + (size_t)k * NB * g.lds;
-      const int rlo = c0 + nb + NB;  // first row of block b+2
-      const int rhi = min(n - 1, c0 + nb - 1 + g.kd);
-      const int t = threadIdx.x - 64;
-      const int fw = t >> 5, gr = lane >> 2, gc = lane & 3;
-      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-      const int nks = rhi >= rlo ? (rhi - rlo + 4) >> 2 : 0;
-      for (int ks = fw; ks < nks; ks += kFarThreads / 32) {
-        const int row = rlo + 4 * ks + gc;
-        int sl = sx + 4 * ks + gc;
-        if (sl >= g.nx) sl -= g.nx;
-        const double xv = (gr == 0 && row <= rhi) ? bw[sl] : 0.0;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int col = 8 * u + gr;
-          const int off = row - c0 - col;
-          const bool in = col < nb && row <= rhi && off <= g.kd;
-          const double av = blk[col * g.lds + (in ? off : 0)];
-          dmma884(acc[u][0], acc[u][1], in ? av : 0.0, xv);
-        }
-      }
-      if (gc == 0) {
-        part[fw * NB + gr] = acc[0][0];
-        part[fw * NB + 8 + gr] = acc[1][0];
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kFarThreads) : "memory");
-      if (t < 32) {
-        const int i = t & 15;
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < kFarThreads / 32; ++w) sum += part[w * NB + i];
-        // c_b for the chain (which applies M_b^T itself, in parallel with its G_b^T product)
-        if (t < NB) tbuf[(b & 1) * NB + t] = t < nb ? yb[k * NB + t] - sum : 0.0;
-      }
-    };
-    // chain: x_b = M_b^T c_b - G_b^T x_{b+1} (lane (i, h): half h of columns i of M and G, the
-    // two products in parallel), to the x ring and to rhs
-    auto chain = [&](int b, int xb) {  // xb = ring slot of row b*NB
-      const int c0 = b * NB, nb = min(NB, n - c0);
-      const int i = lane & 15, h = lane >> 4;
-      double a0 = 0.0, a1 = 0.0, m0 = 0.0, m1 = 0.0;
-      {
-        // t_b = M_b^T c_b (c_b from the far warps), half h of column i of M
-        const double* M = mslot(b) + (8 * h) * kLDD + i;  // M(8h + jj, i)
-        const double* cv = tbuf + (b & 1) * NB + 8 * h;
-#pragma unroll
-        for (int jj = 0; jj < 8; jj += 2) {
-          m0 = fma(M[jj * kLDD], cv[jj], m0);
-          m1 = fma(M[(jj + 1) * kLDD], cv[jj + 1], m1);
-        }
-      }
-      if (b + 1 < nblk) {
-        const double* G = mslot(b) + NB * kLDD + (8 * h) * kLDD + i;  // G(8h + jj, i)
-        int sx = xb + nb + 8 * h;  // row c0 + nb + 8h
-        if (sx >= g.nx) sx -= g.nx;
-#pragma unroll
-        for (int jj = 0; jj < 8; jj += 2) {
-          int s0 = sx + jj, s1 = sx + jj + 1;
-          if (s0 >= g.nx) s0 -= g.nx;
-          if (s1 >= g.nx) s1 -= g.nx;
-          const int r0 = c0 + nb + 8 * h + jj;
-          const double x0 = r0 < n ? bw[s0] : 0.0, x1 = r0 + 1 < n ? bw[s1] : 0.0;
-          a0 = fma(G[jj * kLDD], x0, a0);
-          a1 = fma(G[(jj + 1) * kLDD], x1, a1);
-        }
-      }
-      double s = (m0 + m1) - (a0 + a1);
-      s += __shfl_xor_sync(kFull, s, 16);
-      const double x = s;
-      if (lane < nb) {
-        int sr = xb + lane;
-        if (sr >= g.nx) sr -= g.nx;
-        bw[sr] = x;
-        rhs[c0 + lane] = x;
-      }
-    };
-    // ring positions, tracked incrementally: kb = block b's buffer, xb = ring slot of row b*NB
-    auto dec = [&](int v, int by, int mod) { v -= by; return v < 0 ? v + mod : v; };
-    int kb = (nblk - 1) % nbuf;
-    int xb = ((nblk - 1) * NB) % g.nx;
-    for (int d = 0; d < nbuf; ++d) issue(nblk - 1 - d, dec(kb, d, nbuf));
-    const int tb = nblk + 1;  // trace rows after the factorization's
-    // prologue: M/G of the last two blocks, c/t of the last one
-    wait_buf(kb);
-    __syncthreads();
-    if (warp == 1) invert(nblk - 1, kb);
-    __syncthreads();
-    if (nblk >= 2) wait_buf(dec(kb, 1, nbuf));
-    __syncthreads();
-    if (warp == 1 && nblk >= 2) invert(nblk - 2, dec(kb, 1, nbuf));
-    if (warp >= 2) {
-      const int nbl = n - (nblk - 1) * NB;
-      int sx = xb + nbl + NB;
-      while (sx >= g.nx) sx -= g.nx;
-      far_t(nblk - 1, kb, sx);
-    }
-    __syncthreads();
-    issue(nblk - 1 - nbuf, kb);  // the last block is done (inverter, far): its buffer moves on
-    for (int b = nblk - 1; b >= 0; --b) {
-      const int km1 = dec(kb, 1, nbuf), km2 = dec(kb, 2, nbuf);
-      if (threadIdx.x < 32) trace_stamp(tb + b, 0);
-      if (b >= 2) wait_buf(km2);  // block b-2 (the inverter's), per thread
-      if (threadIdx.x < 32) trace_stamp(tb + b, 1);
-      if (warp == 0) {
-        chain(b, xb);
-        trace_stamp(tb + b, 2);
-        // block b is done (far at b+1, inverter at b+2): its buffer takes block b - nbuf, issued
-        // here by the chain warp (it has slack) rather than after the barrier
-        if (fast && b <= nblk - 2) issue(b - nbuf, kb);
-      } else if (warp == 1) {
-        if (b >= 2) invert(b - 2, km2);
-        trace_stamp(tb + b, 4);
-      } else if (b >= 1) {
-        int sxf = xb + NB;  // row (b-1)*NB + NB + NB = c0 + NB
-        if (sxf >= g.nx) sxf -= g.nx;
-        far_t(b - 1, km1, sxf);
-        if (warp == 2) trace_stamp(tb + b, 5);
-      }
-      __syncthreads();
-      if (threadIdx.x < 32) trace_stamp(tb + b, 3);
-      if (!fast && b <= nblk - 2) issue(b - nbuf, kb);  // element-wise fallback: all threads
-      kb = km1;
-      xb = dec(xb, NB, g.nx);
-    }
-    // buffer mbarrier phases advanced by this matrix: one completion per block
-    __syncthreads();
-    if (threadIdx.x < nbuf) {
-      int cnt = 0;
-      for (int b = threadIdx.x; b < nblk; b += nbuf) ++cnt;
-      bphase[threadIdx.x] = (bphase[threadIdx.x] + (unsigned)cnt) & 1u;
     }
     __syncthreads();
   }

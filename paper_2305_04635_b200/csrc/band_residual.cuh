@@ -39,9 +39,14 @@ __device__ __forceinline__ void block_sum2(double& a, double& b) {
   }
 }
 
+// blockIdx.y = matrix of a batch (a + y*stride_a, l + y*stride_l); partials of matrix y at
+// partial + 2*gridDim.x*y.
 __global__ void __launch_bounds__(kResidThreads)
 band_residual_kernel(int n, int kd, const double* __restrict__ a, int lda, const double* __restrict__ l, int ldl,
-                     double* __restrict__ partial) {
+                     double* __restrict__ partial, int64_t stride_a = 0, int64_t stride_l = 0) {
+  a += (int64_t)blockIdx.y * stride_a;
+  l += (int64_t)blockIdx.y * stride_l;
+  partial += (size_t)2 * gridDim.x * blockIdx.y;
   double num = 0.0, den = 0.0;
   for (int j = blockIdx.x; j < n; j += gridDim.x) {
     for (int d = threadIdx.x; d <= kd; d += kResidThreads) {
@@ -73,8 +78,13 @@ band_residual_kernel(int n, int kd, const double* __restrict__ a, int lda, const
   }
 }
 
-__global__ void band_residual_finish(const double* __restrict__ partial, int blocks, double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+// one thread per matrix (batch of `count`): partials summed in block order
+__global__ void band_residual_finish(const double* __restrict__ partial, int blocks, double* __restrict__ out,
+                                     int count = 1) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  if (y >= count) return;
+  partial += (size_t)2 * blocks * y;
+  out += y;
   double num = 0.0, den = 0.0;
   for (int i = 0; i < blocks; ++i) {
     num += partial[2 * i];

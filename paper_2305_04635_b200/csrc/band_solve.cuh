@@ -23,8 +23,10 @@ __device__ int first_nonpositive_diag(const double* __restrict__ ab, int n, int 
   if (threadIdx.x == 0) s_bad = INT_MAX;
   __syncthreads();
   int mine = INT_MAX;
-  for (int j = threadIdx.x; j < n; j += kCtaThreads)
-    if (ab[(int64_t)j * ldab] <= 0.0) { mine = j; break; }
+  // no early exit: the loads of a thread are independent and overlap (one latency, not n/T)
+#pragma unroll 8
+  for (int j = threadIdx.x; j < n; j += blockDim.x)
+    if (ab[(int64_t)j * ldab] <= 0.0 && mine == INT_MAX) mine = j;
   if (mine != INT_MAX) atomicMin(&s_bad, mine);
   __syncthreads();
   const int r = s_bad;
@@ -127,6 +129,28 @@ __device__ void band_backward(const double* __restrict__ ab, int n, int kd, int 
     }
     __syncthreads();
   }
+}
+
+// Solve for wide bands (the streamed ring does not fit): one CTA per right-hand side,
+// blockIdx.x = matrix * nrhs + rhs; column r of matrix m at b0 + m*stride_b + r*ldb.
+// Matrices with skip[m] != 0 (failed factorization) are left untouched.
+__global__ void __launch_bounds__(kCtaThreads)
+pbtrs_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t ldb, int64_t stride_b, int nrhs, int n, int kd,
+             int ldab, int32_t* info, const int32_t* skip) {
+  const int z = blockIdx.x, mat = z / nrhs, r = z - mat * nrhs;
+  if (skip && skip[mat] != 0) return;
+  const double* ab = ab0 + (int64_t)mat * stride_ab;
+  double* b = b0 + (int64_t)mat * stride_b + (int64_t)r * ldb;
+  if (!skip) {
+    const int bad = first_nonpositive_diag(ab, n, ldab);
+    if (bad != INT_MAX) {
+      if (threadIdx.x == 0 && r == 0) info[mat] = bad + 1;
+      return;
+    }
+  }
+  band_forward(ab, n, kd, ldab, b);
+  band_backward(ab, n, kd, ldab, b);
+  if (threadIdx.x == 0 && r == 0) info[mat] = 0;
 }
 
 }  // namespace bcg

@@ -13,120 +13,42 @@
 #include "../../include/bandchol_b200.h"
 #include "band_cta.cuh"
 #include "band_solve.cuh"
+#include "band_sweep.cuh"
 #include "band_residual.cuh"
 #include "band_multi.cuh"
 
 namespace bcg {
 
 // One CTA per matrix (grid-stride over the batch).
-template <int NB, bool kSolve, int KD>
+template <int NB, int KD>
 __global__ void __launch_bounds__(kCtaThreads, 2)
-pbtrf_cta_kernel(double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int batch, CtaGeom g,
-                 int32_t* info) {
+pbtrf_cta_kernel(double* ab0, int64_t stride_ab, int batch, CtaGeom g, int32_t* info) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) unsigned long long bars[1 + 16];
-  __shared__ unsigned bphase[16];
+  __shared__ __align__(8) unsigned long long bars[1];
   __shared__ int s_sp[kCtaWarps];
   __shared__ __align__(8) unsigned long long sig[4];
-  if (threadIdx.x < 17) mbar_init(&bars[threadIdx.x], 1);
-  if (threadIdx.x < 16) bphase[threadIdx.x] = 0;
+  if (threadIdx.x == 0) mbar_init(&bars[0], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   unsigned phase = 0;
   for (int mat = blockIdx.x; mat < batch; mat += gridDim.x) {
-    CtaBand<NB, kSolve, KD> w{g};
+    CtaBand<NB, KD> w{g};
     w.bars = bars;
-    w.bphase = bphase;
     w.phase = phase;
     w.set_roles(s_sp);
     w.tr = (blockIdx.x == 0 && mat == 0) ? g_trace : nullptr;
     w.ab = ab0 + (int64_t)mat * stride_ab;
-    w.rhs = kSolve ? b0 + (int64_t)mat * stride_b : nullptr;
     double* p = smem;
     w.win = p; p += (size_t)g.nslot * g.lds;
-    w.P = p; p += cta_panel_doubles(NB, g, kSolve);
+    w.P = p; p += cta_panel_doubles(NB, g);
     w.D = p; p += 2 * NB * (NB + 4);
-    w.Dinv = w.D + NB * (NB + 4);
-    w.lbuf = p; p += NB;
+    w.lbuf = p;
     w.sig = sig;
-    w.bw = kSolve ? p : nullptr;
-    if (kSolve) p += g.nslot;
-    w.yb = kSolve ? p : nullptr;
     const int fail = w.factor();
     phase = w.phase;
-    if (kSolve && fail < 0) w.backward();
     if (threadIdx.x == 0) info[mat] = fail < 0 ? 0 : fail + 1;
     __syncthreads();
   }
-}
-
-// Standalone solve, one CTA per right-hand side: forward and backward sweeps stream the
-// factor's column blocks through a 5-buffer shared ring (see CtaBand::forward/backward).
-__global__ void __launch_bounds__(kCtaThreads, 2)
-pbtrs_cta_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int nrhs, CtaGeom g,
-                 int32_t* info, const int32_t* skip) {
-  constexpr int NB = 16;
-  extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) unsigned long long bars[1 + 16];
-  __shared__ unsigned bphase[16];
-  if (threadIdx.x < 17) mbar_init(&bars[threadIdx.x], 1);
-  if (threadIdx.x < 16) bphase[threadIdx.x] = 0;
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  const int z = blockIdx.x, mat = z / nrhs;
-  if (skip && skip[mat] != 0) return;  // (after a batched factorization: this one failed, keep its info)
-  const double* abm = ab0 + (int64_t)mat * stride_ab;
-  const int bad = first_nonpositive_diag(abm, g.n, g.ldab);
-  if (bad != INT_MAX) {
-    if (threadIdx.x == 0 && z % nrhs == 0) info[mat] = bad + 1;
-    return;
-  }
-  CtaBand<NB, true> w{g};
-  w.bars = bars;
-  w.bphase = bphase;
-  w.ab = const_cast<double*>(abm);
-  w.rhs = b0 + (int64_t)z * stride_b;
-  w.tr = (z == 0) ? g_trace : nullptr;
-  double* p = smem;
-  w.win = p; p += (size_t)g.nslot * g.lds;
-  w.P = p; p += cta_panel_doubles(NB, g, true);
-  w.D = p; p += 2 * NB * (NB + 4);
-  w.Dinv = w.D + NB * (NB + 4);
-  w.lbuf = p; p += NB;
-  w.bw = p; p += g.nx;
-  w.yb = p;
-  w.init_fast();
-  w.forward();
-  w.backward();
-  if (threadIdx.x == 0 && z % nrhs == 0) info[mat] = 0;
-}
-
-__global__ void __launch_bounds__(kCtaThreads)
-pbtrs_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int nrhs, int n, int kd,
-             int ldab, int32_t* info) {
-  const int z = blockIdx.x;
-  const double* ab = ab0 + (int64_t)(z / nrhs) * stride_ab;
-  double* b = b0 + (int64_t)z * stride_b;
-  const int bad = first_nonpositive_diag(ab, n, ldab);
-  if (bad != INT_MAX) {
-    if (threadIdx.x == 0) info[z / nrhs] = bad + 1;
-    return;
-  }
-  band_forward(ab, n, kd, ldab, b);
-  band_backward(ab, n, kd, ldab, b);
-  if (threadIdx.x == 0 && z % nrhs == 0) info[z / nrhs] = 0;
-}
-
-// Solve step of the unfused dpbsv path: matrices whose factorization failed keep info.
-__global__ void __launch_bounds__(kCtaThreads)
-pbtrs_after_factor_kernel(const double* ab0, int64_t stride_ab, double* b0, int64_t stride_b, int n, int kd,
-                          int ldab, const int32_t* info) {
-  const int z = blockIdx.x;
-  if (info[z] != 0) return;
-  const double* ab = ab0 + (int64_t)z * stride_ab;
-  double* b = b0 + (int64_t)z * stride_b;
-  band_forward(ab, n, kd, ldab, b);
-  band_backward(ab, n, kd, ldab, b);
 }
 
 }  // namespace bcg
@@ -152,37 +74,40 @@ int cuda_status(cudaError_t e, const char* what) {
   return (int)e;
 }
 
-int smem_optin() {
-  static int v = -1;
-  if (v < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 48 * 1024;
+// Device attributes of the CURRENT device (the one every launch goes to), cached per
+// device ordinal.
+constexpr int kMaxDevices = 64;
+
+int device_attr(cudaDeviceAttr attr, int fallback, int (&cache)[kMaxDevices]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return fallback;
+  int v = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, attr, dev) != cudaSuccess || v <= 0) return fallback;
+    __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
   }
   return v;
+}
+
+int smem_optin() {
+  static int cache[kMaxDevices];
+  return device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 48 * 1024, cache);
 }
 
 int sm_count() {
-  static int v = -1;
-  if (v < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
-  }
-  return v;
+  static int cache[kMaxDevices];
+  return device_attr(cudaDevAttrMultiProcessorCount, 148, cache);
 }
 
-bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb, bool solve) {
+bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb) {
   bcg::CtaGeom g;
   g.n = n;
   g.kd = kd;
   g.ldab = ldab;
   g.lds = ldab;  // ring slots mirror the global columns (bulk copies move whole columns)
   int ns = kd + nb;
-  if (solve && ns < 5 * nb) ns = 5 * nb;  // backward-sweep prefetch ring: 5 blocks
   if (ns & 1) ++ns;
   g.nslot = ns;
-  g.nx = ns;
   // >= kd rows, = 4 (mod 16): conflict-free DMMA fragment loads.  The tile GEMM reads (and
   // discards) up to 12 rows past kd, i.e. into the next column or the buffer after P.
   int pld = kd + ((4 - kd % 16) + 16) % 16;
@@ -192,39 +117,29 @@ bcg::CtaGeom make_geom(int n, int kd, int ldab, int nb, bool solve) {
 
 // Block size for the one-CTA-per-matrix kernel (NB = 16) when its window fits two
 // CTAs per SM, else one; 0 if the window does not fit at all.
-int cta_block(int n, int kd, int ldab, bool solve, bcg::CtaGeom* out) {
+int cta_block(int n, int kd, int ldab, bcg::CtaGeom* out) {
   const size_t limit = (size_t)smem_optin();
   const size_t half = 113 * 1024 - 512;  // two CTAs per SM: 228 KB less 1 KB per CTA and the static smem
   for (size_t cap : {half, limit}) {
     const int nb = 16;
-    bcg::CtaGeom g = make_geom(n, kd, ldab, nb, solve);
-    if (bcg::cta_smem_bytes(nb, g, solve) > cap) continue;
+    bcg::CtaGeom g = make_geom(n, kd, ldab, nb);
+    if (bcg::cta_smem_bytes(nb, g) > cap) continue;
     *out = g;
     return nb;
   }
   return 0;
 }
 
-template <int NB, bool S>
-int launch_cta_t(double* ab, int64_t sab, double* b, int64_t sb, int batch, const bcg::CtaGeom& g, int32_t* info,
-                 cudaStream_t st) {
-  const size_t smem = bcg::cta_smem_bytes(NB, g, S);
-  // the C5 band width gets a compile-time-geometry instantiation of the factorization (constant
-  // strides: 3.67 -> 3.51 ms for 1024 matrices); measured slower for the fused solve and for
-  // kd = 50, which keep the runtime geometry
-  auto k = (!S && bcg::GeomFixed<100, S>::matches(g)) ? bcg::pbtrf_cta_kernel<NB, S, S ? 0 : 100>
-                                                       : bcg::pbtrf_cta_kernel<NB, S, 0>;
+int launch_cta(double* ab, int64_t sab, int batch, const bcg::CtaGeom& g, int32_t* info, cudaStream_t st) {
+  constexpr int NB = 16;
+  const size_t smem = bcg::cta_smem_bytes(NB, g);
+  // the C5 band width gets a compile-time-geometry instantiation (constant strides: 3.67 ->
+  // 3.51 ms for 1024 matrices); other widths keep the runtime geometry
+  auto k = bcg::GeomFixed<100>::matches(g) ? bcg::pbtrf_cta_kernel<NB, 100> : bcg::pbtrf_cta_kernel<NB, 0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
-  k<<<batch, bcg::kCtaThreads, smem, st>>>(ab, sab, b, sb, batch, g, info);
+  k<<<batch, bcg::kCtaThreads, smem, st>>>(ab, sab, batch, g, info);
   return cuda_status(cudaGetLastError(), "pbtrf_cta_kernel launch");
-}
-
-int launch_cta(double* ab, int64_t sab, double* b, int64_t sb, int batch, int nb, const bcg::CtaGeom& g,
-               int32_t* info, bool solve, cudaStream_t st) {
-  (void)nb;  // 16: the smallest block has the shortest per-step chain and window
-  if (solve) return launch_cta_t<16, true>(ab, sab, b, sb, batch, g, info, st);
-  return launch_cta_t<16, false>(ab, sab, b, sb, batch, g, info, st);
 }
 
 int check_geom(int64_t n, int64_t kd, int64_t ldab) {
@@ -236,9 +151,70 @@ int check_geom(int64_t n, int64_t kd, int64_t ldab) {
 
 }  // namespace
 
+// Streamed solve (band_sweep.cuh): a ring of nbuf 16-column buffers, the deepest ring that
+// keeps two CTAs per SM (else one); 0 when not even four buffers fit (wide bands), where
+// the direct-from-L2 kernel runs instead.
+static bcg::SweepGeom sweep_geom(int n, int kd, int ldab, int R) {
+  bcg::SweepGeom g;
+  g.n = n;
+  g.kd = kd;
+  g.ldab = ldab;
+  g.nblk = (n + 15) / 16;
+  g.nx = 16 * ((kd + 16 + 15) / 16);
+  g.nbuf = 0;
+  // per-CTA budgets for two and one CTAs per SM (228 KB less 1 KB per CTA and the static
+  // shared memory)
+  const size_t two = (size_t)(112 * 1024), one = (size_t)smem_optin() - 1024;
+  for (size_t cap : {two, one}) {
+    for (int nb = 8; nb >= 4; --nb) {
+      g.nbuf = nb;
+      if (bcg::sweep_smem_doubles(g, R) * sizeof(double) <= cap) return g;
+    }
+  }
+  g.nbuf = 0;
+  return g;
+}
+
+static int sweep_r(int64_t nrhs) { return nrhs <= 1 ? 1 : nrhs <= 2 ? 2 : nrhs <= 4 ? 4 : nrhs <= 8 ? 8 : 16; }
+
+template <int R>
+static int launch_sweep_t(const double* ab, int64_t sab, double* b, int64_t ldb, int64_t sb, int nrhs, int batch,
+                          const bcg::SweepGeom& g, int32_t* info, cudaStream_t st, const int32_t* skip) {
+  const size_t smem = bcg::sweep_smem_doubles(g, R) * sizeof(double);
+  auto k = bcg::pbtrs_sweep_kernel<R>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(pbtrs_sweep)");
+  const int groups = (nrhs + R - 1) / R;
+  k<<<(unsigned)((int64_t)batch * groups), bcg::kSweepThreads, smem, st>>>(ab, sab, b, ldb, sb, nrhs, groups, g, info,
+                                                                           skip, skip ? 0 : 1);
+  return cuda_status(cudaGetLastError(), "pbtrs_sweep_kernel launch");
+}
+
+// Solve `batch` systems, each with nrhs right-hand sides (column r of matrix m at
+// b + m*sb + r*ldb).  skip (device, may be NULL): matrices with skip[m] != 0 are left alone
+// (their factorization failed); with skip the diagonal check is not repeated.
+static int launch_solve(const double* ab, int64_t sab, double* b, int64_t ldb, int64_t sb, int nrhs, int batch,
+                        int n, int kd, int ldab, int32_t* info, cudaStream_t st, const int32_t* skip = nullptr) {
+  const int R = sweep_r(nrhs);
+  const bcg::SweepGeom g = sweep_geom(n, kd, ldab, R);
+  if (g.nbuf) {
+    switch (R) {
+      case 1: return launch_sweep_t<1>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
+      case 2: return launch_sweep_t<2>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
+      case 4: return launch_sweep_t<4>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
+      case 8: return launch_sweep_t<8>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
+      default: return launch_sweep_t<16>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
+    }
+  }
+  // wide bands: one CTA per right-hand side straight from L2
+  bcg::pbtrs_kernel<<<(unsigned)((int64_t)batch * nrhs), bcg::kCtaThreads, 0, st>>>(ab, sab, b, ldb, sb, nrhs, n, kd,
+                                                                                     ldab, info, skip);
+  return cuda_status(cudaGetLastError(), "pbtrs_kernel launch");
+}
+
 extern "C" {
 
-int bcg_version(void) { return 100; }
+int bcg_version(void) { return 200; }
 
 const char* bcg_last_error(void) { return g_err; }
 
@@ -246,7 +222,7 @@ const char* bcg_last_error(void) { return g_err; }
 // whole-GPU dataflow kernel (which needs the caller's workspace).
 static bool single_uses_multi(int n, int kd, int ldab) {
   bcg::CtaGeom g;
-  return cta_block(n, kd, ldab, false, &g) == 0 || bcg::use_multi(n, kd);
+  return cta_block(n, kd, ldab, &g) == 0 || bcg::use_multi(n, kd);
 }
 
 size_t bcg_dpbtrf_workspace_size(int64_t n, int64_t kd, int64_t ldab) {
@@ -268,27 +244,34 @@ int bcg_dpbtrf(int64_t n, int64_t kd, double* ab, int64_t ldab, int32_t* info, v
     return bcg::launch_multi(ab, (int)n, (int)kd, (int)ldab, info, workspace, sm_count(), st, g_err, sizeof g_err);
   }
   bcg::CtaGeom g;
-  const int nb = cta_block((int)n, (int)kd, (int)ldab, false, &g);
-  return launch_cta(ab, 0, nullptr, 0, 1, nb, g, info, false, st);
+  cta_block((int)n, (int)kd, (int)ldab, &g);
+  return launch_cta(ab, 0, 1, g, info, st);
 }
 
 // Batched matrices whose window does not fit one CTA: one whole-GPU factorization
-// after another, with a stream-ordered workspace.
+// after another, on the caller's workspace (cleared by every launch, stream-ordered).
 static int batched_multi(int n, int kd, int ldab, double* ab, int64_t stride_ab, int batch, int32_t* info,
-                         cudaStream_t st) {
-  const size_t need = bcg::multi_workspace_bytes(n, kd);
-  void* ws = nullptr;
-  if (int r = cuda_status(cudaMallocAsync(&ws, need, st), "cudaMallocAsync(workspace)")) return r;
+                         void* ws, cudaStream_t st) {
   int rc = 0;
   for (int i = 0; i < batch && rc == 0; ++i)
     rc = bcg::launch_multi(ab + (int64_t)i * stride_ab, n, kd, ldab, info + i, ws, sm_count(), st, g_err,
                            sizeof g_err);
-  cudaFreeAsync(ws, st);
   return rc;
 }
 
+static bool batched_uses_multi(int n, int kd, int ldab) {
+  bcg::CtaGeom g;
+  return cta_block(n, kd, ldab, &g) == 0;
+}
+
+size_t bcg_dpbtrf_batched_workspace_size(int64_t n, int64_t kd, int64_t ldab, int64_t batch) {
+  if (check_geom(n, kd, ldab) != 0 || batch <= 0) return 0;
+  if (!batched_uses_multi((int)n, (int)kd, (int)ldab)) return 0;
+  return bcg::multi_workspace_bytes((int)n, (int)kd);
+}
+
 int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, int64_t batch,
-                       int32_t* info, void* stream) {
+                       int32_t* info, void* workspace, size_t workspace_bytes, void* stream) {
   if (int r = check_geom(n, kd, ldab)) return r;
   if (!ab) return fail_arg(3, "ab is NULL");
   if (stride_ab < ldab * n) return fail_arg(5, "stride_ab < ldab*n");
@@ -296,17 +279,20 @@ int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t 
   if (!info) return fail_arg(7, "info is NULL");
   if (batch == 0) return 0;
   bcg::CtaGeom g;
-  const int nb = cta_block((int)n, (int)kd, (int)ldab, false, &g);
-  if (nb == 0) return batched_multi((int)n, (int)kd, (int)ldab, ab, stride_ab, (int)batch, info, (cudaStream_t)stream);
-  return launch_cta(ab, stride_ab, nullptr, 0, (int)batch, nb, g, info, false, (cudaStream_t)stream);
+  if (cta_block((int)n, (int)kd, (int)ldab, &g) == 0) {
+    const size_t need = bcg::multi_workspace_bytes((int)n, (int)kd);
+    if (!workspace || workspace_bytes < need)
+      return fail_arg(8, "workspace of %zu bytes required (got %zu)", need, workspace_bytes);
+    return batched_multi((int)n, (int)kd, (int)ldab, ab, stride_ab, (int)batch, info, workspace,
+                         (cudaStream_t)stream);
+  }
+  return launch_cta(ab, stride_ab, (int)batch, g, info, (cudaStream_t)stream);
 }
 
-static int launch_solve(const double* ab, int64_t sab, double* b, int64_t sb, int nrhs, int64_t blocks, int n,
-                        int kd, int ldab, int32_t* info, cudaStream_t st, const int32_t* skip = nullptr);
-static bool solve_streamed(int n, int kd, int ldab);
 
 int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, double* b,
-                      int64_t stride_b, int64_t batch, int32_t* info, void* stream) {
+                      int64_t stride_b, int64_t batch, int32_t* info, void* workspace, size_t workspace_bytes,
+                      void* stream) {
   if (int r = check_geom(n, kd, ldab)) return r;
   if (!ab) return fail_arg(3, "ab is NULL");
   if (stride_ab < ldab * n) return fail_arg(5, "stride_ab < ldab*n");
@@ -315,54 +301,13 @@ int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t s
   if (batch < 0 || batch > INT_MAX) return fail_arg(8, "batch out of range");
   if (!info) return fail_arg(9, "info is NULL");
   if (batch == 0) return 0;
-  cudaStream_t st = (cudaStream_t)stream;
-  bcg::CtaGeom g;
-  // kd >= 32: the pipelined factorization alone, then the streamed two-sweep solve (skipping
-  // failed matrices) -- measured faster than fusing the forward sweep into the pivot's chain
-  // (C5 1024: 3.51 + 2.30 ms vs 5.99 ms)
-  if (kd >= 32 && cta_block((int)n, (int)kd, (int)ldab, false, &g) && solve_streamed((int)n, (int)kd, (int)ldab)) {
-    if (int rc = bcg_dpbtrf_batched(n, kd, ab, ldab, stride_ab, batch, info, stream)) return rc;
-    return launch_solve(ab, stride_ab, b, stride_b, 1, batch, (int)n, (int)kd, (int)ldab, info, st, info);
-  }
-  const int nb = cta_block((int)n, (int)kd, (int)ldab, true, &g);
-  if (nb) return launch_cta(ab, stride_ab, b, stride_b, (int)batch, nb, g, info, true, st);
-  // no fused variant for this geometry: factor, then solve (solve skips failed matrices)
-  int rc = bcg_dpbtrf_batched(n, kd, ab, ldab, stride_ab, batch, info, stream);
-  if (rc) return rc;
-  bcg::pbtrs_after_factor_kernel<<<(unsigned)batch, bcg::kCtaThreads, 0, st>>>(ab, stride_ab, b, stride_b, (int)n,
-                                                                             (int)kd, (int)ldab, info);
-  return cuda_status(cudaGetLastError(), "pbtrs_after_factor_kernel launch");
-}
-
-// Streamed solve (shared-memory ring of 5-7 column blocks) when it fits, else the
-// direct-from-L2 kernel.
-static bcg::CtaGeom solve_geom(int n, int kd, int ldab) {
-  bcg::CtaGeom g = make_geom(n, kd, ldab, 16, true);
-  g.nx = ((kd + 48) + 1) & ~1;      // rows in flight: kd + NB, plus the entering block
-  // block buffers for the streamed sweeps: 7 (deeper prefetch) when two CTAs still fit per
-  // SM, else 5
-  g.nslot = 7 * 16;
-  if (bcg::cta_smem_bytes(16, g, true) > (size_t)(113 * 1024 - 512)) g.nslot = 5 * 16;
-  return g;
-}
-
-static bool solve_streamed(int n, int kd, int ldab) {
-  return bcg::cta_smem_bytes(16, solve_geom(n, kd, ldab), true) <= (size_t)smem_optin();
-}
-
-static int launch_solve(const double* ab, int64_t sab, double* b, int64_t sb, int nrhs, int64_t blocks, int n,
-                        int kd, int ldab, int32_t* info, cudaStream_t st, const int32_t* skip) {
-  const bcg::CtaGeom g = solve_geom(n, kd, ldab);
-  const size_t smem = bcg::cta_smem_bytes(16, g, true);
-  if (smem <= (size_t)smem_optin()) {
-    auto k = bcg::pbtrs_cta_kernel;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(pbtrs_cta)");
-    k<<<(unsigned)blocks, bcg::kCtaThreads, smem, st>>>(ab, sab, b, sb, nrhs, g, info, skip);
-    return cuda_status(cudaGetLastError(), "pbtrs_cta_kernel launch");
-  }
-  bcg::pbtrs_kernel<<<(unsigned)blocks, bcg::kCtaThreads, 0, st>>>(ab, sab, b, sb, nrhs, n, kd, ldab, info);
-  return cuda_status(cudaGetLastError(), "pbtrs_kernel launch");
+  // the batched factorization, then the solve, which skips the matrices whose factorization
+  // failed (their b stays untouched, as LAPACK dpbsv leaves B when info > 0).  Fusing the
+  // forward sweep into the factorization's pivot chain measured slower.
+  if (int rc = bcg_dpbtrf_batched(n, kd, ab, ldab, stride_ab, batch, info, workspace, workspace_bytes, stream))
+    return rc;
+  return launch_solve(ab, stride_ab, b, n, stride_b, 1, (int)batch, (int)n, (int)kd, (int)ldab, info,
+                      (cudaStream_t)stream, info);
 }
 
 int bcg_dpbtrs(int64_t n, int64_t kd, const double* ab, int64_t ldab, double* b, int64_t ldb, int64_t nrhs,
@@ -374,20 +319,27 @@ int bcg_dpbtrs(int64_t n, int64_t kd, const double* ab, int64_t ldab, double* b,
   if (nrhs > 1 && ldb < n) return fail_arg(6, "ldb < n");
   if (!info) return fail_arg(8, "info is NULL");
   if (nrhs == 0) return 0;
-  return launch_solve(ab, 0, b, ldb, (int)nrhs, nrhs, (int)n, (int)kd, (int)ldab, info, (cudaStream_t)stream);
+  return launch_solve(ab, 0, b, ldb, 0, (int)nrhs, 1, (int)n, (int)kd, (int)ldab, info, (cudaStream_t)stream);
 }
 
 int bcg_dpbtrs_batched(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab, double* b,
                        int64_t stride_b, int64_t batch, int32_t* info, void* stream) {
+  return bcg_dpbtrs_batched_nrhs(n, kd, ab, ldab, stride_ab, b, n, stride_b, 1, batch, info, stream);
+}
+
+int bcg_dpbtrs_batched_nrhs(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab, double* b,
+                            int64_t ldb, int64_t stride_b, int64_t nrhs, int64_t batch, int32_t* info, void* stream) {
   if (int r = check_geom(n, kd, ldab)) return r;
   if (!ab) return fail_arg(3, "ab is NULL");
   if (stride_ab < ldab * n) return fail_arg(5, "stride_ab < ldab*n");
   if (!b) return fail_arg(6, "b is NULL");
-  if (stride_b < n) return fail_arg(7, "stride_b < n");
-  if (batch < 0 || batch > INT_MAX) return fail_arg(8, "batch out of range");
-  if (!info) return fail_arg(9, "info is NULL");
-  if (batch == 0) return 0;
-  return launch_solve(ab, stride_ab, b, stride_b, 1, batch, (int)n, (int)kd, (int)ldab, info,
+  if (nrhs > 1 && ldb < n) return fail_arg(7, "ldb < n");
+  if (stride_b < (nrhs > 1 ? ldb * (nrhs - 1) + n : n)) return fail_arg(8, "stride_b smaller than one matrix's rhs");
+  if (nrhs < 0 || nrhs > INT_MAX) return fail_arg(9, "nrhs out of range");
+  if (batch < 0 || batch > INT_MAX || batch * ((nrhs + 15) / 16) > INT_MAX) return fail_arg(10, "batch out of range");
+  if (!info) return fail_arg(11, "info is NULL");
+  if (batch == 0 || nrhs == 0) return 0;
+  return launch_solve(ab, stride_ab, b, ldb, stride_b, (int)nrhs, (int)batch, (int)n, (int)kd, (int)ldab, info,
                       (cudaStream_t)stream);
 }
 
@@ -470,4 +422,34 @@ extern "C" int bcg_band_residual(int64_t n, int64_t kd, const double* a, int64_t
   bcg::band_residual_kernel<<<blocks, bcg::kResidThreads, 0, st>>>((int)n, (int)kd, a, (int)lda, l, (int)ldl, part);
   bcg::band_residual_finish<<<1, 32, 0, st>>>(part, blocks, result);
   return cuda_status(cudaGetLastError(), "band_residual_kernel launch");
+}
+
+// batched: kResidBatchBlocks blocks per matrix
+static constexpr int kResidBatchBlocks = 4;
+
+extern "C" size_t bcg_band_residual_batched_workspace_size(int64_t batch) {
+  return batch < 0 ? 0 : (size_t)batch * kResidBatchBlocks * 2 * sizeof(double);
+}
+
+extern "C" int bcg_band_residual_batched(int64_t n, int64_t kd, const double* a, int64_t lda, int64_t stride_a,
+                                         const double* l, int64_t ldl, int64_t stride_l, int64_t batch,
+                                         double* result, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int r = check_geom(n, kd, lda)) return r;
+  if (!a) return fail_arg(3, "a is NULL");
+  if (stride_a < lda * n) return fail_arg(5, "stride_a < lda*n");
+  if (!l) return fail_arg(6, "l is NULL");
+  if (ldl < kd + 1 || ldl > INT_MAX / 2) return fail_arg(7, "ldl=%lld < kd+1", (long long)ldl);
+  if (stride_l < ldl * n) return fail_arg(8, "stride_l < ldl*n");
+  if (batch < 0 || batch > 65535) return fail_arg(9, "batch out of range [0, 65535]");
+  if (!result) return fail_arg(10, "result is NULL");
+  if (batch == 0) return 0;
+  if (!workspace || workspace_bytes < bcg_band_residual_batched_workspace_size(batch))
+    return fail_arg(11, "workspace smaller than bcg_band_residual_batched_workspace_size(batch)");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = (double*)workspace;
+  bcg::band_residual_kernel<<<dim3(kResidBatchBlocks, (unsigned)batch), bcg::kResidThreads, 0, st>>>(
+      (int)n, (int)kd, a, (int)lda, l, (int)ldl, part, stride_a, stride_l);
+  bcg::band_residual_finish<<<(unsigned)((batch + 127) / 128), 128, 0, st>>>(part, kResidBatchBlocks, result,
+                                                                              (int)batch);
+  return cuda_status(cudaGetLastError(), "band_residual_kernel launch (batched)");
 }

@@ -59,24 +59,51 @@ def _torch():
     return torch
 
 
+def _stream_for(torch, device, stream):
+    """The launch stream: `stream`, else the current stream of `device` (never of whatever
+    device happens to be current)."""
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if stream.device != device:
+        raise ShapeMismatch(f"stream is on {stream.device}, tensors on {device}")
+    return stream
+
+
 def _stream_handle(torch, stream) -> int:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
 
 
-_workspaces: dict = {}
+class _on_device:
+    """Make `device` current for the C-ABI call (the library launches on the current
+    device; every pointer passed must live there)."""
+
+    def __init__(self, torch, device):
+        self.guard = torch.cuda.device(device)
+
+    def __enter__(self):
+        self.guard.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        return self.guard.__exit__(*exc)
 
 
-def _workspace(torch, n: int, kd: int, ldab: int):
-    """Zero-filled per-device workspace for the multi-CTA kernel (kept between calls)."""
+def _same_device(device, **tensors) -> None:
+    for name, t in tensors.items():
+        if t is not None and t.device != device:
+            raise ShapeMismatch(f"{name} is on {t.device}, ab on {device}")
+
+
+def _workspace(torch, n: int, kd: int, ldab: int, device, stream):
+    """Workspace of the multi-CTA kernel, allocated per call in stream order on `stream`
+    (torch's caching allocator makes this cheap); the kernel launch clears it, so calls on
+    different streams never share flags."""
     need = int(_lib.load().bcg_dpbtrf_workspace_size(n, kd, ldab))
     if need == 0:
         return None, 0
-    dev = torch.cuda.current_device()
-    ws = _workspaces.get(dev)
-    if ws is None or ws.numel() < need:
-        ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
-        _workspaces[dev] = ws
+    with torch.cuda.stream(stream):
+        ws = torch.empty(need, dtype=torch.uint8, device=device)
     return ws, need
 
 
@@ -121,10 +148,14 @@ def dpbtrf_device(ab, n: int, kd: int, ldab: int, info=None, stream=None):
     torch = _torch()
     _dev(ab, torch, torch.float64, ldab * n, "ab")
     info = _info(torch, info, 1, ab.device)
-    ws, need = _workspace(torch, n, kd, ldab)
-    rc = _lib.load().bcg_dpbtrf(n, kd, ab.data_ptr(), ldab, info.data_ptr(),
-                                ws.data_ptr() if ws is not None else None, need,
-                                _stream_handle(torch, stream))
+    _same_device(ab.device, info=info)
+    with _on_device(torch, ab.device):
+        st = _stream_for(torch, ab.device, stream)
+        ws, need = _workspace(torch, n, kd, ldab, ab.device, st)
+        rc = _lib.load().bcg_dpbtrf(n, kd, ab.data_ptr(), ldab, info.data_ptr(),
+                                    ws.data_ptr() if ws is not None else None, need, st.cuda_stream)
+        if ws is not None:
+            ws.record_stream(st)
     _lib.check(rc, "bcg_dpbtrf")
     return info
 
@@ -134,8 +165,19 @@ def dpbtrf_batched_device(ab, n: int, kd: int, ldab: int, batch: int, info=None,
     torch = _torch()
     _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
     info = _info(torch, info, batch, ab.device)
-    rc = _lib.load().bcg_dpbtrf_batched(n, kd, ab.data_ptr(), ldab, ldab * n, batch,
-                                        info.data_ptr(), _stream_handle(torch, stream))
+    _same_device(ab.device, info=info)
+    with _on_device(torch, ab.device):
+        st = _stream_for(torch, ab.device, stream)
+        lib = _lib.load()
+        need = int(lib.bcg_dpbtrf_batched_workspace_size(n, kd, ldab, batch))
+        ws = None
+        if need:
+            with torch.cuda.stream(st):
+                ws = torch.empty(need, dtype=torch.uint8, device=ab.device)
+        rc = lib.bcg_dpbtrf_batched(n, kd, ab.data_ptr(), ldab, ldab * n, batch, info.data_ptr(),
+                                    ws.data_ptr() if ws is not None else None, need, st.cuda_stream)
+        if ws is not None:
+            ws.record_stream(st)
     _lib.check(rc, "bcg_dpbtrf_batched")
     return info
 
@@ -146,33 +188,59 @@ def dpbtrs_device(ab, n: int, kd: int, ldab: int, b, nrhs: int = 1, info=None, s
     _dev(ab, torch, torch.float64, ldab * n, "ab")
     _dev(b, torch, torch.float64, n * nrhs, "b")
     info = _info(torch, info, 1, ab.device)
-    rc = _lib.load().bcg_dpbtrs(n, kd, ab.data_ptr(), ldab, b.data_ptr(), n, nrhs,
-                                info.data_ptr(), _stream_handle(torch, stream))
+    _same_device(ab.device, b=b, info=info)
+    with _on_device(torch, ab.device):
+        st = _stream_for(torch, ab.device, stream)
+        rc = _lib.load().bcg_dpbtrs(n, kd, ab.data_ptr(), ldab, b.data_ptr(), n, nrhs,
+                                    info.data_ptr(), st.cuda_stream)
     _lib.check(rc, "bcg_dpbtrs")
     return info
 
 
-def dpbtrs_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=None, stream=None):
-    """Solve every system of a factored batch (L from dpbtrf_batched_device) in place in b."""
+def dpbtrs_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, nrhs: int = 1, info=None,
+                          stream=None):
+    """Solve every system of a factored batch (L from dpbtrf_batched_device) in place in b:
+    matrix i has nrhs right-hand sides, b[i] of shape (nrhs, n)."""
     torch = _torch()
     _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
-    _dev(b, torch, torch.float64, n * batch, "b")
+    _dev(b, torch, torch.float64, n * nrhs * batch, "b")
     info = _info(torch, info, batch, ab.device)
-    rc = _lib.load().bcg_dpbtrs_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
-                                        batch, info.data_ptr(), _stream_handle(torch, stream))
+    _same_device(ab.device, b=b, info=info)
+    with _on_device(torch, ab.device):
+        st = _stream_for(torch, ab.device, stream)
+        lib = _lib.load()
+        if nrhs == 1:
+            rc = lib.bcg_dpbtrs_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
+                                        batch, info.data_ptr(), st.cuda_stream)
+        else:
+            rc = lib.bcg_dpbtrs_batched_nrhs(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
+                                             n * nrhs, nrhs, batch, info.data_ptr(), st.cuda_stream)
     _lib.check(rc, "bcg_dpbtrs_batched")
     return info
 
 
 def dpbsv_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=None, stream=None):
-    """Factor + solve of `batch` systems: ab -> L, b -> x (bcg_dpbsv_batched: for kd >= 32 the
-    pipelined factorization then the streamed solve, else one fused kernel)."""
+    """Factor + solve of `batch` systems: ab -> L, b -> x (bcg_dpbsv_batched: the batched
+    factorization, then the streamed solve, which skips failed matrices and leaves their b
+    untouched)."""
     torch = _torch()
     _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
     _dev(b, torch, torch.float64, n * batch, "b")
     info = _info(torch, info, batch, ab.device)
-    rc = _lib.load().bcg_dpbsv_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
-                                       batch, info.data_ptr(), _stream_handle(torch, stream))
+    _same_device(ab.device, b=b, info=info)
+    with _on_device(torch, ab.device):
+        st = _stream_for(torch, ab.device, stream)
+        lib = _lib.load()
+        need = int(lib.bcg_dpbtrf_batched_workspace_size(n, kd, ldab, batch))
+        ws = None
+        if need:
+            with torch.cuda.stream(st):
+                ws = torch.empty(need, dtype=torch.uint8, device=ab.device)
+        rc = lib.bcg_dpbsv_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n,
+                                   batch, info.data_ptr(), ws.data_ptr() if ws is not None else None,
+                                   need, st.cuda_stream)
+        if ws is not None:
+            ws.record_stream(st)
     _lib.check(rc, "bcg_dpbsv_batched")
     return info
 
@@ -187,12 +255,41 @@ def band_residual_device(a, l, n: int, kd: int, lda: int, ldl: int, out=None, st
     if out is None:
         out = torch.empty(1, dtype=torch.float64, device=a.device)
     _dev(out, torch, torch.float64, 1, "out")
-    need = int(lib.bcg_band_residual_workspace_size())
-    ws = torch.empty(need // 8 + 1, dtype=torch.float64, device=a.device)
-    rc = lib.bcg_band_residual(n, kd, a.data_ptr(), lda, l.data_ptr(), ldl, out.data_ptr(), ws.data_ptr(),
-                               need, _stream_handle(torch, stream))
+    _same_device(a.device, l=l, out=out)
+    with _on_device(torch, a.device):
+        st = _stream_for(torch, a.device, stream)
+        need = int(lib.bcg_band_residual_workspace_size())
+        with torch.cuda.stream(st):
+            ws = torch.empty(need // 8 + 1, dtype=torch.float64, device=a.device)
+        rc = lib.bcg_band_residual(n, kd, a.data_ptr(), lda, l.data_ptr(), ldl, out.data_ptr(), ws.data_ptr(),
+                                   need, st.cuda_stream)
+        ws.record_stream(st)
     _lib.check(rc, "bcg_band_residual")
     return out
+
+
+def band_residual_batched_device(a, l, n: int, kd: int, lda: int, ldl: int, batch: int, out=None,
+                                 stream=None):
+    """Per-matrix backward error of a batch (a: original matrices, l: their factors, rows
+    of lda*n / ldl*n doubles); returns a CUDA float64 tensor of `batch` residuals."""
+    torch = _torch()
+    lib = _lib.load()
+    _dev(a, torch, torch.float64, lda * n * batch, "a")
+    _dev(l, torch, torch.float64, ldl * n * batch, "l")
+    if out is None:
+        out = torch.empty(max(batch, 1), dtype=torch.float64, device=a.device)
+    _dev(out, torch, torch.float64, batch, "out")
+    _same_device(a.device, l=l, out=out)
+    with _on_device(torch, a.device):
+        st = _stream_for(torch, a.device, stream)
+        need = int(lib.bcg_band_residual_batched_workspace_size(batch))
+        with torch.cuda.stream(st):
+            ws = torch.empty(need // 8 + 1, dtype=torch.float64, device=a.device)
+        rc = lib.bcg_band_residual_batched(n, kd, a.data_ptr(), lda, lda * n, l.data_ptr(), ldl, ldl * n, batch,
+                                           out.data_ptr(), ws.data_ptr(), need, st.cuda_stream)
+        ws.record_stream(st)
+    _lib.check(rc, "bcg_band_residual_batched")
+    return out[:batch]
 
 
 def residual_norm(original, factor) -> float:
@@ -308,21 +405,45 @@ def factor_solve_batched(data: np.ndarray, rhs: np.ndarray, dim: int, bandwidth:
 
 def solve_batched(factors: np.ndarray, rhs: np.ndarray, dim: int, bandwidth: int,
                   lead_dim: int | None = None) -> np.ndarray:
-    """x_i = solve_with_factor(L_i, rhs_i) for every matrix; returns x (batch, dim)."""
+    """x_i = solve_with_factor(L_i, rhs_i) for every matrix.  rhs (batch, dim) -> x (batch, dim),
+    or (batch, nrhs, dim) -> X (batch, nrhs, dim): every right-hand side of a matrix is served
+    by the same pass over its factor (bcg_dpbtrs_batched_nrhs)."""
     ld = bandwidth + 1 if lead_dim is None else lead_dim
     a = _batch_array(factors, dim, ld)
     r = np.ascontiguousarray(rhs, dtype=np.float64)
-    if r.shape != (a.shape[0], dim):
-        raise ShapeMismatch(f"rhs must be ({a.shape[0]}, {dim})")
+    if r.ndim == 2 and r.shape == (a.shape[0], dim):
+        nrhs = 1
+    elif r.ndim == 3 and r.shape[0] == a.shape[0] and r.shape[2] == dim:
+        nrhs = r.shape[1]
+    else:
+        raise ShapeMismatch(f"rhs must be ({a.shape[0]}, {dim}) or ({a.shape[0]}, nrhs, {dim})")
     torch = _torch()
     dab = torch.from_numpy(a).to("cuda")
     db = torch.from_numpy(r.copy()).to("cuda")
-    info = dpbtrs_batched_device(dab, dim, bandwidth, ld, db, a.shape[0]).cpu().numpy()
+    info = dpbtrs_batched_device(dab, dim, bandwidth, ld, db, a.shape[0], nrhs=nrhs).cpu().numpy()
     bad = np.nonzero(info)[0]
     if bad.size:
         err = SingularFactor(f"matrix {bad[0]}: factor diagonal not positive at column {info[bad[0]] - 1}")
         err.matrix = int(bad[0])
         raise err
+    return db.cpu().numpy()
+
+
+def solve_many(factor, rhs) -> np.ndarray:
+    """Several right-hand sides against one factor: rhs (nrhs, N) -> X (nrhs, N), one pass
+    over L per 16 right-hand sides (the repeated solves of an interior-point iteration,
+    PAPER.md:20).  Same checks and errors as solve_with_factor (core.py:216-240)."""
+    n, k, ld, data = check_matrix(factor)
+    b = np.asarray(rhs, dtype=np.float64)
+    if b.ndim != 2 or b.shape[1] != n:
+        raise ShapeMismatch(f"rhs shape {b.shape} is not (nrhs, {n})")
+    torch = _torch()
+    dab = torch.from_numpy(data).to("cuda")
+    db = torch.from_numpy(np.ascontiguousarray(b).copy()).to("cuda")
+    info = dpbtrs_device(dab, n, k, ld, db, nrhs=b.shape[0])
+    info_h = int(info.item())
+    if info_h > 0:
+        raise SingularFactor(f"factor diagonal not positive at column {info_h - 1}")
     return db.cpu().numpy()
 
 
@@ -340,10 +461,10 @@ def library_version() -> int:
 
 
 __all__ = [
-    "band_residual_device", "residual_norm",
+    "band_residual_device", "band_residual_batched_device", "residual_norm",
     "TraceEvent", "dpbtrf_device", "dpbtrf_batched_device", "dpbtrs_device", "dpbtrs_batched_device",
     "dpbsv_batched_device", "factor_blocked_serial", "factor_blocked_parallel", "solve_with_factor",
-    "factor_batched", "factor_solve_batched", "solve_batched", "library_version",
+    "factor_batched", "factor_solve_batched", "solve_batched", "solve_many", "library_version",
     "BatchedBandSolver", "pinned_empty",
 ]
 
@@ -354,12 +475,7 @@ def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
     """Page-locked host array (so host<->device copies run at full PCIe rate, async)."""
     torch = _torch()
     t = torch.empty(shape, dtype=torch.float64 if dtype == np.float64 else torch.int32, pin_memory=True)
-    arr = t.numpy()
-    _pinned_keepalive[arr.ctypes.data] = t  # the torch tensor owns the pinned pages
-    return arr
-
-
-_pinned_keepalive: dict = {}
+    return t.numpy()  # the ndarray's base is the tensor: it keeps the pinned pages alive
 
 
 class BatchedBandSolver:

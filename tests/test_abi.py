@@ -45,9 +45,17 @@ def test_version_and_argument_validation():
     assert lib.bcg_dpbtrf(10, 3, None, 3, None, None, 0, None) == -4
     assert lib.bcg_dpbtrf(10, 3, None, 4, None, None, 0, None) == -3
     assert b"ab is NULL" in lib.bcg_last_error()
-    assert lib.bcg_dpbtrf_batched(10, 3, ctypes.c_void_p(8), 4, 39, 1, None, None) == -5
+    assert lib.bcg_dpbtrf_batched(10, 3, ctypes.c_void_p(8), 4, 39, 1, None, None, 0, None) == -5
     assert lib.bcg_dpbtrs(10, 3, ctypes.c_void_p(8), 4, None, 10, 1, None, None) == -5
-    assert lib.bcg_dpbsv_batched(10, 3, ctypes.c_void_p(8), 4, 40, ctypes.c_void_p(8), 9, 1, None, None) == -7
+    assert lib.bcg_dpbsv_batched(10, 3, ctypes.c_void_p(8), 4, 40, ctypes.c_void_p(8), 9, 1, None, None, 0,
+                                 None) == -7
+    # multi-rhs batched: ldb < n, then a stride_b that cannot hold nrhs columns
+    assert lib.bcg_dpbtrs_batched_nrhs(10, 3, ctypes.c_void_p(8), 4, 40, ctypes.c_void_p(8), 9, 100, 2, 1,
+                                       None, None) == -7
+    assert lib.bcg_dpbtrs_batched_nrhs(10, 3, ctypes.c_void_p(8), 4, 40, ctypes.c_void_p(8), 10, 19, 2, 1,
+                                       None, None) == -8
+    assert lib.bcg_band_residual_batched(10, 3, ctypes.c_void_p(8), 4, 39, ctypes.c_void_p(8), 4, 40, 1,
+                                         ctypes.c_void_p(8), None, 0, None) == -5
 
 
 def test_error_mapping():
@@ -62,3 +70,7 @@ def test_workspace_query_is_pure():
         ws = lib.bcg_dpbtrf_workspace_size(n, kd, kd + 1)
         assert ws >= 0
     assert lib.bcg_dpbtrf_workspace_size(10, 10, 11) == 0
+    # batched: one CTA per matrix up to the shared-memory window, the whole-GPU kernel beyond
+    assert lib.bcg_dpbtrf_batched_workspace_size(4096, 100, 101, 1024) == 0
+    assert lib.bcg_dpbtrf_batched_workspace_size(20000, 2000, 2001, 2) > 0
+    assert lib.bcg_band_residual_batched_workspace_size(1024) == 1024 * 4 * 2 * 8

@@ -1,6 +1,6 @@
 """Quick device timings of the library entry points (CUDA events), for development.
 
-usage: python tools/timing.py [c5|single|all] [--batch B]
+usage: python tools/timing.py [c5|single|rhs|all] [--batch B]
 """
 import json
 import os
@@ -67,6 +67,29 @@ def c5(batch):
     print(json.dumps({"c5_batch": batch, **out}), flush=True)
 
 
+def rhs_sweep():
+    """Multi-right-hand-side solve: one factor, nrhs = 1..16 (one pass over L per 16), and
+    the batched C5 shape with 1 and 16 right-hand sides per matrix."""
+    n, k = 4096, 100
+    a = generate_spd(n, k, 0)
+    bc.factor_blocked_serial(a)
+    dab = torch.from_numpy(a.data).cuda()
+    out = {}
+    for R in (1, 2, 4, 8, 16, 32):
+        db = torch.from_numpy(np.stack([make_rhs(n, s) for s in range(R)])).cuda()
+        ms, _ = timed(lambda: bc.dpbtrs_device(dab, n, k, k + 1, db, nrhs=R), 5)
+        out[f"single_nrhs{R}_ms"] = ms
+    batch = 1024
+    w = dab.repeat(batch)
+    info = torch.zeros(batch, dtype=torch.int32, device="cuda")
+    for R in (1, 4, 16):
+        db = torch.from_numpy(np.stack([make_rhs(n, s) for s in range(R)])).cuda().repeat(batch, 1)
+        ms, _ = timed(lambda: bc.dpbtrs_batched_device(w, n, k, k + 1, db, batch, nrhs=R, info=info), 3)
+        out[f"batch1024_nrhs{R}_ms"] = ms
+        out[f"batch1024_nrhs{R}_GBs"] = 2 * batch * n * (k + 1) * 8 / (ms * 1e-3) / 1e9
+    print(json.dumps(out), flush=True)
+
+
 def single(tags):
     for tag in tags:
         cfg = CONFIGS[tag]
@@ -94,6 +117,8 @@ if __name__ == "__main__":
         c5(batch)
     if what in ("single", "all"):
         single(["C1", "C2", "C3", "C4"])
+    if what in ("rhs", "all"):
+        rhs_sweep()
 
 
 def trace(tag):
@@ -207,37 +232,42 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_bwd":
     trace_bwd(296)
 
 
-def trace_solve(batch=1):
-    """Phase breakdown of the streamed standalone solve (block 0): forward and backward."""
+def trace_solve(batch=1, nrhs=1):
+    """Per-step phase breakdown of the streamed solve (band_sweep.cuh, CTA 0), SM cycles."""
     from paper_2305_04635_b200 import _lib
     n, k = 4096, 100
     a = np.stack([generate_spd(n, k, s).data for s in range(min(batch, 8))])
     a = np.concatenate([a] * ((batch + 7) // 8))[:batch]
     a0 = torch.from_numpy(a).cuda()
     bc.dpbtrf_batched_device(a0, n, k, k + 1, batch)
-    b0 = torch.from_numpy(np.stack([make_rhs(n, s) for s in range(batch)])).cuda()
+    b0 = torch.from_numpy(np.stack([make_rhs(n, s) for s in range(batch * nrhs)])).cuda()
     nblk = n // 16
     buf = torch.zeros(1 + 8 * (2 * nblk + 4), dtype=torch.int64, device="cuda")
     lib = _lib.load()
+    bc.dpbtrs_batched_device(a0, n, k, k + 1, b0.clone(), batch, nrhs=nrhs)
+    torch.cuda.synchronize()
     lib.bcg_set_trace(buf.data_ptr(), buf.numel() * 8)
-    wb = b0.clone()
-    bc.dpbtrs_batched_device(a0, n, k, k + 1, wb, batch)
+    bc.dpbtrs_batched_device(a0, n, k, k + 1, b0.clone(), batch, nrhs=nrhs)
     torch.cuda.synchronize()
     lib.bcg_set_trace(None, 0)
-    t = buf.cpu().numpy()[1:].reshape(-1, 8).astype(np.float64)
-    f = t[1:nblk - 1]
-    bw = t[nblk + 1: 2 * nblk + 1]
+    t = buf.cpu().numpy()[1:1 + 8 * 2 * nblk].reshape(2 * nblk, 8).astype(np.float64)
     med = lambda x: float(np.median(x))  # noqa: E731
-    out = {"batch": batch, "fwd_block": med(np.diff(t[:nblk, 0])), "fwd_wait": med(f[:, 1] - f[:, 0]),
-           "fwd_warp0": med(f[:, 2] - f[:, 1]), "fwd_invert": med(f[:, 4] - f[:, 1]),
-           "fwd_far": med(f[:, 5] - f[:, 1]), "fwd_sync": med(f[:, 3] - f[:, 1]),
-           "bwd_block": med(bw[:-1, 0] - bw[1:, 0])}
+    out = {"batch": batch, "nrhs": nrhs}
+    for name, sl in (("fwd", slice(4, nblk - 4)), ("bwd", slice(nblk + 4, 2 * nblk - 4))):
+        u = t[sl]
+        out[name] = {"step": med(np.diff(u[:, 0])), "chain_wait": med(u[:, 1] - u[:, 0]),
+                     "chain_work": med(u[:, 2] - u[:, 1]), "far_work": med(u[:, 4] - u[:, 3]),
+                     "prep_sub": med(u[:, 6] - u[:, 5]), "prep_t": med(u[:, 7] - u[:, 6]),
+                     "t_ready_before_chain": med(u[:, 1] - u[:, 7])}
+    out["fwd"]["far_start_after_ydone"] = med(t[4:nblk - 4, 3] - t[4:nblk - 4, 2])
+    out["total_cycles"] = float(t[-1, 2] - t[0, 0])
     print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_solve":
     trace_solve(1)
     trace_solve(296)
+    trace_solve(1, 16)
 
 
 def trace_la(tag, batch=1, solve=False):
