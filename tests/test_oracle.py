@@ -149,3 +149,49 @@ def test_solve_golden_is_a_solution(golden_meta, small):
     a, x, b = small[f"{name}/A"], small[f"{name}/x"], small[f"{name}/rhs"]
     r = band_matvec(meta["n"], meta["k"], meta["lead_dim"], a, x) - b
     assert np.linalg.norm(r) / np.linalg.norm(b) <= 1e-12
+
+
+def test_blocked_dense_oracle_close_to_reference(golden_meta, small):
+    """oracle.factor_blocked_dense (the C3/C4 full-L checker) against the reference's
+    factor_reference on every small golden case, at several tile sizes."""
+    for name, meta in _cases(golden_meta):
+        n, k, ld = meta["n"], meta["k"], meta["lead_dim"]
+        for nb in (3, 16, 64):
+            a = small[f"{name}/A"].copy()
+            oracle.factor_blocked_dense(n, k, ld, a, nb)
+            assert oracle.max_scaled_diff(n, k, a, ld, small[f"{name}/L_ref"], ld) <= 1e-13, (name, nb)
+            pad = np.ones(ld * n, dtype=bool)  # padding never written
+            for j in range(n):
+                pad[j * ld: j * ld + min(k, n - 1 - j) + 1] = False
+            assert np.array_equal(a[pad], small[f"{name}/A"][pad]), name
+
+
+@pytest.mark.parametrize("tag", ["C2", "C3"])
+def test_blocked_dense_oracle_on_large_samples(golden_meta, large, tag):
+    meta = golden_meta["large"][tag]
+    n, k = meta["n"], meta["k"]
+    a = (generate_spd_wide if meta["wide_diagonal"] else generate_spd)(n, k, meta["seed"])
+    oracle.factor_blocked_dense(n, k, k + 1, a.data)
+    cols = large[f"{tag}/cols"]
+    got = np.stack([a.data[c * (k + 1):(c + 1) * (k + 1)] for c in cols])
+    assert scaled_diff(got, large[f"{tag}/L_blocked_cols"]) <= 1e-12
+
+
+def test_blocked_dense_oracle_failure_column(golden_meta, small):
+    for name, want in golden_meta["failures"].items():
+        a = small[f"{name}/A"].copy()
+        with pytest.raises(oracle.OracleFailure) as err:
+            oracle.factor_blocked_dense(want["n"], want["k"], want["k"] + 1, a, 16)
+        assert err.value.column == want["column"], name
+
+
+def test_plain_batched_is_plain():
+    n, k = 700, 30
+    data = np.stack([generate_spd(n, k, s).data for s in range(6)])
+    data[4, 123 * (k + 1)] = -1.0
+    want = data.copy()
+    info = oracle.factor_plain_batched(n, k, k + 1, data)
+    assert list(info) == [-1, -1, -1, -1, 123, -1]
+    for s in (0, 1, 2, 3, 5):
+        oracle.factor_plain(n, k, k + 1, want[s])
+        assert data[s].tobytes() == want[s].tobytes()
