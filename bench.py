@@ -1,22 +1,24 @@
 """Benchmark: fp64 banded Cholesky GFLOP/s (n*kd*(kd+3)) and % of the FP64/HBM roofline.
 
 Default workload (config.workload "C5"): BASELINE.json configs[4], a batch of 1,024
-independent SPD band matrices n=4096, kd=100, factor + one-RHS band solve per matrix --
-the one config that partitions across GPUs (each rank factors its own batch of
-1,024 matrices with distinct seeds, no collective on the data path; per-GPU work is
-fixed as N grows => "weak" scaling, value = matrices of all ranks / max-over-ranks time).  `--config C1..C4` benches a single-matrix
-config instead.  A step = one factor+solve pass over the whole batch (C5: bcg_dpbsv_batched,
-i.e. the pipelined factorization kernel then the streamed solve kernel) or one
-factorization (+ solve for C2) of the matrix, inputs resident in HBM; a fresh
-device-to-device copy of the pristine inputs is made before every step OUTSIDE the
-timed events (it also flushes L2: 3.4 GB > 126 MB).
+independent SPD band matrices n=4096, kd=100, factor + one-RHS band solve per matrix.
+Multi-GPU is STRONG scaling exactly as C5 defines it: the fixed global batch (1,024, or
+--batch B) is partitioned contiguously over the N ranks (sharding.shard), no collective on
+the data path, value = all ranks' matrices / max-over-ranks time.  `--config C1..C4`
+benches a single-matrix config instead (replicas per GPU).  A step = one factor+solve pass
+over the rank's shard through bcg_dpbsv_batched (the factorization kernel, then the
+streamed solve kernel), inputs resident in HBM; a fresh device-to-device copy of the
+pristine inputs is made before every step OUTSIDE the timed events (it also flushes L2:
+3.4 GB > 126 MB).  The two kernels are also timed separately (CUDA events on the launching
+stream) for the per-kernel roofline: the factorization against the FP64 peak (the dominant
+kernel, `roofline`), the solve against HBM (`roofline.kernels.solve`).
 
 Rank 0 prints ONE JSON line (driver contract).  `--impl reference` times the
 reference's own CPU implementation (the unmodified bandchol package installed in
 baseline/_ref, blocked-serial engine, one process per host core) on a bounded sample
 of the same workload.
 
-Launch: python bench.py [--gpus N --steps K --warmup W]; N>1 under torchrun.
+Launch: python bench.py [--gpus N --steps K --warmup W --batch B]; N>1 under torchrun.
 """
 
 from __future__ import annotations
@@ -230,8 +232,8 @@ def run_reference_arm(args) -> int:
     line = {
         "metric": "fp64 banded Cholesky GFLOP/s (n*kd*(kd+3))", "impl": "reference", "value": value,
         "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "scaling": "weak", "dtype": "f64", "data": "synthetic (reference generator)",
-        "config": config_block(tag, world),
+        "higher_is_better": True, "scaling": "strong", "dtype": "f64", "data": "synthetic (reference generator)",
+        "config": config_block(tag, world, global_batch(tag, args.batch)),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": res["cores"], "kind": res["kind"],
                          "sample": res["sample"]},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -241,13 +243,22 @@ def run_reference_arm(args) -> int:
     return 0
 
 
-def config_block(tag: str, world: int) -> dict:
+def global_batch(tag: str, override: int | None) -> int:
     cfg = CONFIGS[tag]
-    return {"workload": tag, "n": cfg.dim, "kd": cfg.bandwidth, "batch": cfg.batch,
-            "global_batch": cfg.batch * world if cfg.batch > 1 else 1,
+    if cfg.batch <= 1:
+        return 1
+    return int(override) if override else cfg.batch
+
+
+def config_block(tag: str, world: int, batch: int) -> dict:
+    cfg = CONFIGS[tag]
+    per = [shard(batch, r, world)[1] - shard(batch, r, world)[0] for r in range(world)]
+    return {"workload": tag, "n": cfg.dim, "kd": cfg.bandwidth, "batch": batch,
+            "global_batch": batch if cfg.batch > 1 else world,
+            "batch_per_gpu": max(per) if cfg.batch > 1 else 1,
             "factor_and_solve": cfg.solve, "wide_diagonal": cfg.wide_diagonal,
-            "parallelism": (f"batch-sharded x{world} ({cfg.batch} matrices per GPU)" if cfg.batch > 1
-                            else "single matrix per GPU (replicas)"),
+            "parallelism": (f"batch-sharded x{world} (strong: {batch} matrices split {'/'.join(map(str, per))})"
+                            if cfg.batch > 1 else "single matrix per GPU (replicas)"),
             "l2": "inputs > L2 and fresh D2D copy between steps (flushes L2)"}
 
 
@@ -268,26 +279,28 @@ def run_gpu_arm(args) -> int:
     tag = args.config
     cfg = CONFIGS[tag]
     n, kd, ld = cfg.dim, cfg.bandwidth, cfg.bandwidth + 1
-    # weak scaling: the global batch is cfg.batch per rank; rank r owns the contiguous
-    # shard [r*batch, (r+1)*batch) of it (global seeds), no collective on the data path
-    lo, hi = shard(cfg.batch * world, rank, world) if cfg.batch > 1 else (0, 1)
+    batch = global_batch(tag, args.batch)
+    # strong scaling: rank r owns the contiguous shard [lo, hi) of the fixed global batch
+    # (global seeds), no collective on the data path; single-matrix configs: replicas
+    lo, hi = shard(batch, rank, world) if cfg.batch > 1 else (0, 1)
     nb = hi - lo
-    ab_host = bc.pinned_empty((nb, ld * n))
-    b_host = bc.pinned_empty((nb, n))
+    ab_host = bc.pinned_empty((max(nb, 1), ld * n))
+    b_host = bc.pinned_empty((max(nb, 1), n))
     generate_batch(tag, range(lo, hi), ab_host, b_host)
     a0 = torch.from_numpy(ab_host).cuda()
     b0 = torch.from_numpy(b_host).cuda()
     work_a = torch.empty_like(a0)
     work_b = torch.empty_like(b0)
-    info = torch.zeros(nb, dtype=torch.int32, device="cuda")
+    info = torch.zeros(max(nb, 1), dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream()
 
     def step():
+        """One pass of the product path over this rank's shard; returns our launches."""
+        if nb == 0:
+            return 0
         if cfg.batch > 1:
             bc.dpbsv_batched_device(work_a, n, kd, ld, work_b, nb, info=info, stream=stream)
-            # bcg_dpbsv_batched: kd >= 32 runs the pipelined factorization, then the streamed
-            # solve (two kernels); narrower bands one fused kernel
-            return 2 if kd >= 32 else 1
+            return 2  # bcg_dpbsv_batched: the factorization kernel, then the solve kernel
         bc.dpbtrf_device(work_a[0], n, kd, ld, info=info, stream=stream)
         if cfg.solve:
             bc.dpbtrs_device(work_a[0], n, kd, ld, work_b[0], info=info, stream=stream)
@@ -321,19 +334,41 @@ def run_gpu_arm(args) -> int:
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    per_ms = [s.elapsed_time(e) for s, e in ev]
+    per_ms = [s_.elapsed_time(e_) for s_, e_ in ev]
     total_ms = sum(per_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    flops_total = cfg.batch * world * n * kd * (kd + 3)  # every rank's matrices (replicas for C1-C4)
+    n_mat = batch if cfg.batch > 1 else world  # every rank's matrices (replicas for C1-C4)
+    flops_total = n_mat * n * kd * (kd + 3)
     value = flops_total * args.steps / (max_ms * 1e-3) / 1e9  # GFLOP/s, whole job
 
+    # the two kernels of a step timed apart (same stream, CUDA events): factorization, solve
+    fac_ms, sol_ms = [], []
+    for i in range(args.steps if nb else 0):
+        refresh()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        if cfg.batch > 1:
+            bc.dpbtrf_batched_device(work_a, n, kd, ld, nb, info=info, stream=stream)
+        else:
+            bc.dpbtrf_device(work_a[0], n, kd, ld, info=info, stream=stream)
+        e1.record(stream)
+        if cfg.solve:
+            if cfg.batch > 1:
+                bc.dpbtrs_batched_device(work_a, n, kd, ld, work_b, nb, info=info, stream=stream)
+            else:
+                bc.dpbtrs_device(work_a[0], n, kd, ld, work_b[0], info=info, stream=stream)
+        e2.record(stream)
+        torch.cuda.synchronize()
+        fac_ms.append(e0.elapsed_time(e1))
+        sol_ms.append(e1.elapsed_time(e2))
+
     # end to end through the public API with host buffers (pinned), per rank shard
-    solver = bc.BatchedBandSolver(nb, n, kd, chunks=16) if cfg.batch > 1 else None
-    e2e_ab = bc.pinned_empty((nb, ld * n))
-    e2e_b = bc.pinned_empty((nb, n))
+    solver = bc.BatchedBandSolver(nb, n, kd, chunks=16) if cfg.batch > 1 and nb else None
+    e2e_ab = bc.pinned_empty((max(nb, 1), ld * n))
+    e2e_b = bc.pinned_empty((max(nb, 1), n))
     e2e_times = []
     for i in range(args.warmup + args.steps):
         np.copyto(e2e_ab, ab_host)
@@ -345,7 +380,7 @@ def run_gpu_arm(args) -> int:
         s_ev.record()
         if solver is not None:
             solver.factor_solve(e2e_ab, e2e_b, check=False)
-        else:
+        elif cfg.batch <= 1:
             m = bc.BandedMatrix(n, kd, data=e2e_ab[0])
             bc.factor_blocked_serial(m)
             if cfg.solve:
@@ -361,41 +396,56 @@ def run_gpu_arm(args) -> int:
     h2d = nb * (ld * n + n) * 8 if cfg.batch > 1 else (ld * n + (n if cfg.solve else 0)) * 8
     d2h = h2d
 
-    # roofline: FP64 pipe (probe) vs HBM (MEASURED_PEAKS.json), BASELINE byte model
+    # roofline of the dominant kernel (the factorization: FP64-bound) from its own CUDA-event
+    # time; the solve against HBM (it reads L twice); the whole step for reference
     pk = ctypes_double()
     import ctypes
     _lib.check(_lib.load().bcg_probe_fp64_peak(ctypes.byref(pk)), "bcg_probe_fp64_peak")
     fp64_peak = pk.value * 1e3  # GFLOP/s
     hbm, hbm_src = measured_hbm_gbs()
-    launch_ms = total_ms / args.steps  # one dominant launch per step (C5: the fused kernel)
-    flops_rank = nb * n * kd * (kd + 3)
-    bytes_rank = nb * 16 * n * (kd + 1)
+    mats = max(nb, 1)
+    flops_rank = mats * n * kd * (kd + 3)
+    bytes_rank = mats * 16 * n * (kd + 1)        # factorization: band read + written once
+    solve_bytes = mats * 16 * n * (kd + 1)       # solve: band read twice
+    f_ms = statistics.median(fac_ms) if fac_ms else float("nan")
+    s_ms = statistics.median(sol_ms) if (sol_ms and cfg.solve) else 0.0
+    step_ms = max_ms / args.steps
     t_fp = flops_rank / (fp64_peak * 1e9)
     t_hbm = bytes_rank / (hbm * 1e9)
     bound = "fp64" if t_fp >= t_hbm else "hbm"
     if bound == "fp64":
-        achieved = flops_rank / (launch_ms * 1e-3) / 1e12
+        achieved = flops_rank / (f_ms * 1e-3) / 1e12
         peak, unit = fp64_peak / 1e3, "TFLOP/s"
     else:
-        achieved = bytes_rank / (launch_ms * 1e-3) / 1e9
+        achieved = bytes_rank / (f_ms * 1e-3) / 1e9
         peak, unit = hbm, "GB/s"
-    kernel_key = "bcg::pbtrf_cta_kernel" if cfg.batch > 1 else "bcg_dpbtrf"
+    kernels = {"factor": {"ms": f_ms, "tflops": flops_rank / (f_ms * 1e-3) / 1e12,
+                          "frac_fp64": flops_rank / (f_ms * 1e-3) / 1e9 / fp64_peak}}
+    if cfg.solve:
+        kernels["solve"] = {"ms": s_ms, "gbs": solve_bytes / (s_ms * 1e-3) / 1e9,
+                            "frac_hbm": solve_bytes / (s_ms * 1e-3) / 1e9 / hbm}
+    t_step_roof = max(t_fp, t_hbm) + (solve_bytes / (hbm * 1e9) if cfg.solve else 0.0)
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                "traffic": ncu_traffic(tag), "t_roof_ms": max(t_fp, t_hbm) * 1e3,
-                "roofline_frac_of_step": max(t_fp, t_hbm) * 1e3 / launch_ms,
+                "kernel": "factorization (pbtrf_cta_kernel)" if cfg.batch > 1 else "factorization",
+                "traffic": ncu_traffic(f"{tag}_factor" if cfg.batch > 1 else tag), "kernels": kernels,
+                "step_frac": t_step_roof * 1e3 / step_ms,
+                "step_roof_ms": t_step_roof * 1e3,
                 "peak_source": f"fp64: bcg_probe_fp64_peak DFMA loop (live); hbm: {hbm_src} {hbm:.1f} GB/s",
-                "algorithmic": f"flops n*kd*(kd+3) x {nb} matrices; bytes 16*n*(kd+1) x {nb}"}
+                "algorithmic": (f"factor: flops n*kd*(kd+3), bytes 16*n*(kd+1) x {mats} matrices; solve: "
+                                f"bytes 16*n*(kd+1) x {mats} (L read twice)")}
     line = {
         "metric": "fp64 banded Cholesky GFLOP/s (n*kd*(kd+3))", "value": value, "unit": "GFLOP/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (reference generator, seeds 0..batch-1)",
-        "config": config_block(tag, world), "roofline": roofline, "clocks": clk,
+        "config": config_block(tag, world, batch), "roofline": roofline, "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": float(te.item()) / args.steps, "path": "BatchedBandSolver.factor_solve (pinned host)"
-                if solver is not None else "factor_blocked_serial + solve_with_factor (host numpy)"},
+                if cfg.batch > 1 else "factor_blocked_serial + solve_with_factor (host numpy)"},
         "gpu_launches": launches,
     }
+    if rank == 0 and world == 1 and cfg.batch > 1 and not args.skip_others:
+        line["shards"] = shard_times(bc, work_a, work_b, a0, b0, n, kd, ld, nb, step_ms)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))
         sample = min(cfg.batch, max(1, cores)) if cfg.batch > 1 else 1
@@ -407,6 +457,31 @@ def run_gpu_arm(args) -> int:
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def shard_times(bc, work_a, work_b, a0, b0, n, kd, ld, batch, full_ms) -> dict:
+    """The per-GPU shard of an N-GPU strong-scaling run (batch/N matrices), timed on this GPU:
+    what each rank of a 2/4/8-GPU run computes, and the efficiency T1 / (N * T_N) it implies
+    (no collective on the data path, so a rank's time is its shard's time)."""
+    import torch
+    out = {}
+    info = torch.zeros(batch, dtype=torch.int32, device="cuda")
+    for g in (2, 4, 8):
+        m = batch // g
+        ts = []
+        for i in range(6):
+            work_a[:m].copy_(a0[:m])
+            work_b[:m].copy_(b0[:m])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            bc.dpbsv_batched_device(work_a[:m], n, kd, ld, work_b[:m], m, info=info[:m])
+            e1.record()
+            torch.cuda.synchronize()
+            if i:
+                ts.append(e0.elapsed_time(e1))
+        t = statistics.median(ts)
+        out[f"gpus{g}"] = {"matrices": m, "ms": t, "efficiency": full_ms / (g * t)}
+    return out
 
 
 def ctypes_double():
@@ -463,6 +538,9 @@ def main(argv=None) -> int:
     p.add_argument("--config", choices=tuple(CONFIGS), default="C5")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--skip-others", action="store_true")
+    p.add_argument("--batch", type=int, default=None,
+                   help="global batch of the batched config (default: C5's 1,024); --batch 128 on one "
+                        "GPU is the per-GPU load of the 8-GPU run")
     args = p.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 untimed warm-up steps

@@ -1,11 +1,10 @@
 """Batch partitioning across ranks (one process per GPU) for the batched band solver.
 
-BASELINE.json config C5 partitions batches of independent systems over 1/2/4/8 GPUs with
-no collective on the data path.  `shard` gives each rank a contiguous
-slice of a global batch; the bench runs weak scaling -- a global batch of 1,024 x world
-matrices, i.e. 1,024 per GPU (`shard(1024 * world, rank, world)`).  `gather_rows` is the
-optional gather of per-rank results (e.g. the solutions x) onto every rank, over whatever
-process group torch.distributed was initialised with (NCCL on GPUs, gloo in the CPU tests).
+BASELINE.json config C5 partitions a fixed batch of 1,024 independent systems over 1/2/4/8
+GPUs with no collective on the data path: strong scaling, rank r of N
+owns `shard(1024, r, N)` (1024/N matrices, global seeds).  `gather_rows` is the optional
+gather of per-rank results (e.g. the solutions x) onto every rank, over whatever process
+group torch.distributed was initialised with (NCCL on GPUs, gloo in the CPU tests).
 """
 
 from __future__ import annotations
