@@ -21,7 +21,8 @@
 //              G_b (backward), the same instructions -- then t_b once its inputs are
 //              complete (forward: after y_{b-2} and the far update by y_{b-3}; backward:
 //              after x_{b+2} and the far dot products of block b)
-//   warps 4-6  far: the far update / far dot products (96 threads, no barrier among them)
+//   warps 4-6  far: the far update / far dot products on the FP64 tensor path (DMMA), no
+//              barrier among them
 //   warp 7     producer: waits for a free buffer, loads the block's right-hand-side rows
 //              (forward: b, backward: y) with cp.async and issues the bulk copy of its
 //              16 columns
@@ -41,8 +42,6 @@ constexpr int kSweepWarps = 8;
 constexpr int kSweepThreads = 32 * kSweepWarps;
 constexpr int kSweepPrepWarps = 3;
 constexpr int kSweepFarWarps = 3;
-constexpr int kSweepFarThreads = 32 * kSweepFarWarps;
-constexpr int kSweepFarChunks = kSweepFarThreads / 16;  // backward: row chunks per column
 constexpr int kSweepNP = 6;      // prep ring slots
 constexpr int kSweepNY = 4;      // chain-output / t ring slots (a power of two)
 constexpr int kLinvLd = 18;      // row stride of a prep matrix (16-byte aligned rows)
@@ -63,7 +62,7 @@ __host__ __device__ inline size_t sweep_smem_doubles(const SweepGeom& g, int R) 
          + (size_t)kSweepNP * kPrepSlot         // prep ring
          + (size_t)kSweepNY * 16 * R            // chain outputs
          + (size_t)kSweepNY * 16 * R            // t
-         + (size_t)4 * kSweepFarThreads * R     // backward far partials (a ring of 4 steps)
+         + (size_t)4 * 2 * kSweepFarWarps * 16 * R  // backward far partials (a ring of 4 steps)
          + (size_t)kSweepPrepWarps * 16 * R     // the prep warps' staged vectors
          + (size_t)g.nx * R;                    // accumulator / solution ring
 }
@@ -230,8 +229,8 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   double* prep = rbuf + (size_t)nbuf * 16 * R;        // [NP][2][16][kLinvLd]
   double* ych = prep + kSweepNP * kPrepSlot;          // [NY][16][R]
   double* tbuf = ych + kSweepNY * 16 * R;             // [NY][16][R]
-  double* fpart = tbuf + kSweepNY * 16 * R;           // [4][kSweepFarThreads][R]
-  double* cstage = fpart + 4 * kSweepFarThreads * R;  // [kSweepPrepWarps][16][R]
+  double* fpart = tbuf + kSweepNY * 16 * R;           // [4][kFarParts][16][R]
+  double* cstage = fpart + 4 * 2 * kSweepFarWarps * 16 * R;  // [kSweepPrepWarps][16][R]
   double* ring = cstage + kSweepPrepWarps * 16 * R;   // [nx][R]
 
   if (threadIdx.x < 8) {
@@ -255,13 +254,14 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   const int nsteps = 2 * nblk;
 #ifdef BCG_TRACE
   // phase stamps of CTA 0 (SM cycles), per step s: chain 0 start, 1 waits done, 2 end;
-  // far 3 waits done, 4 done; prep 5 waits done, 6 substitution done, 7 t published.
+  // far 3 waits done, 4 done; prep 5 substitution done, 6 t's waits done, 7 t published.
   // [0] = steps (written once): no global read per stamp.
   unsigned long long* const tr = blockIdx.x == 0 ? g_trace : nullptr;
+  const unsigned long long tcap = g_trace_cap;  // (read once: no global load inside a phase)
   auto stamp = [&](int step, int ph) {
     if (tr && (threadIdx.x & 31) == 0) {
       const unsigned long long idx = 1 + (unsigned long long)step * kTracePhases + ph;
-      if (idx < g_trace_cap) tr[idx] = gtime();
+      if (idx < tcap) tr[idx] = gtime();
     }
   };
   if (tr && threadIdx.x == 0) tr[0] = nsteps;
@@ -272,6 +272,8 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   auto Lbuf = [&](int s) { return Lring + (size_t)(s % nbuf) * 16 * ldab; };
   auto full_wait = [&](int s) { mbar_wait(&full[s % nbuf], (unsigned)(s / nbuf) & 1u); };
   constexpr int RL = R == 1 ? 1 : R / 2;
+  constexpr bool kScalar = R <= 2;  // far work on the FMA pipe (else DMMA)
+  constexpr int kFarParts = kScalar ? 2 * kSweepFarWarps : kSweepFarWarps;  // backward partials per column
   const int i = lane & 15, h = lane >> 4;
   const bool store = R > 1 || h == 0;  // R == 1: both halves compute, only h == 0 stores
   auto rhs_of = [&](int rr) { return R == 1 ? 0 : h + 2 * rr; };
@@ -331,7 +333,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
       full_wait(s);
       if (fwd && s >= 1) full_wait(s - 1);
       if (fwd && s >= 2) full_wait(s - 2);
-      stamp(s, 5);
+      
       const int b = block_of(s), c0 = 16 * b, nb = min(16, n - c0);
       const double* blk = Lbuf(s);
       double* slot = prep + p * kPrepSlot;
@@ -348,21 +350,35 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
         else prep_backward<false>(blk, rows, nb, kd, ldab, j, second, out);
       }
       __syncwarp();
-      stamp(s, 6);
+      stamp(s, 5);
       if (lane == 0) mbar_arrive(&pfull[p]);  // (H_b / G_b for the chain)
       // ---- t_b ----
       // u2 = the second-nearest block's term, which the far warps leave to this warp so the
       // far work has a step more of slack: forward N2_b y_{b-2}, N2_b = L_{b,b-2} (previous-
       // but-one buffer, offsets 32..47); backward N2'_b^T x_{b+2}, N2'_b = L_{b+2,b} (this
-      // buffer, offsets 32..47)
-      const double* rb = rbuf + (size_t)(s % nbuf) * 16 * R;
+      // buffer, offsets 32..47).  Everything that does not depend on the awaited inputs
+      // (indices, the operand rows) is loaded before the waits: only the products and the
+      // staging round trip sit between the inputs and tdone.
+      const int own = s % nbuf;
+      const int q = s % kSweepNY;
+      const double* rb = rbuf + (size_t)own * 16 * R;
+      double* acc = ring + (size_t)((c0 + i) % nx) * R;
+      double* tq = tbuf + q * 16 * R;
+      double mr[16];  // row i of Linv_b (forward) / Linv_b^T (backward)
+      {
+        const double* m = slot + i * kLinvLd;
+#pragma unroll
+        for (int kk = 0; kk < 16; kk += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(m + kk);
+          mr[kk] = t2.x;
+          mr[kk + 1] = t2.y;
+        }
+      }
       double u2[RL];
 #pragma unroll
       for (int rr = 0; rr < RL; ++rr) u2[rr] = 0.0;
       const bool has2 = fwd ? b >= 2 : b + 2 < nblk;
       if (has2) {
-        mbar_wait(&ydone[(s - 2) % kSweepNY], (unsigned)((s - 2) / kSweepNY) & 1u);
-        const double* v2 = ych + ((s - 2) % kSweepNY) * 16 * R;
         double l[16];
         if (fwd) {
           const double* nb2 = Lbuf(s - 2) + 32 + i;  // L(c0+i, c0-32+c) = nb2[c * (ldab-1)]
@@ -383,6 +399,8 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
             l[k] = in ? lv : 0.0;
           }
         }
+        mbar_wait(&ydone[(s - 2) % kSweepNY], (unsigned)((s - 2) / kSweepNY) & 1u);
+        const double* v2 = ych + ((s - 2) % kSweepNY) * 16 * R;
 #pragma unroll
         for (int rr = 0; rr < RL; ++rr) {
           double a4[4] = {0.0, 0.0, 0.0, 0.0};
@@ -394,7 +412,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
       if (fwd) {
         // every far update of block b's rows (by y_{<= b-3}) landed
         if (b >= 3) mbar_wait(&fardone[(s - 3) % kSweepNY], (unsigned)((s - 3) / kSweepNY) & 1u);
-        double* acc = ring + (size_t)((c0 + i) % nx) * R;
+        stamp(s, 6);
         if (store) {
 #pragma unroll
           for (int rr = 0; rr < RL; ++rr) {
@@ -404,25 +422,44 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
           }
         }
       } else {
-        mbar_wait(&fardone[s % kSweepNY], (unsigned)(s / kSweepNY) & 1u);
-        const double* fp = fpart + (size_t)((s & 3) * kSweepFarThreads) * R;
+        mbar_wait(&fardone[q], (unsigned)(s / kSweepNY) & 1u);
+        stamp(s, 6);
+        const double* fp = fpart + (size_t)((s & 3) * kFarParts * 16) * R;
         if (store) {
 #pragma unroll
           for (int rr = 0; rr < RL; ++rr) {
             const int r = rhs_of(rr);
             double f = 0.0;
 #pragma unroll
-            for (int q = 0; q < kSweepFarChunks; ++q) f += fp[(size_t)(q * 16 + i) * R + r];
+            for (int w = 0; w < kFarParts; ++w) f += fp[(size_t)(w * 16 + i) * R + r];
             cv[i * R + r] = (rb[i * R + r] - f) - u2[rr];
           }
         }
       }
       __syncwarp();
+#pragma unroll
+      for (int rr = 0; rr < RL; ++rr) {
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        if (R == 1) {
+#pragma unroll
+          for (int kk = 0; kk < 16; kk += 2) {
+            const double2 c2 = *reinterpret_cast<const double2*>(cv + kk);
+            a4[kk & 3] = fma(mr[kk], c2.x, a4[kk & 3]);
+            a4[(kk + 1) & 3] = fma(mr[kk + 1], c2.y, a4[(kk + 1) & 3]);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(mr[kk], cv[kk * R + rhs_of(rr)], a4[kk & 3]);
+        }
+        if (store) tq[i * R + rhs_of(rr)] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      }
+      __syncwarp();
+      stamp(s, 7);
       if (lane == 0) {
+        mbar_arrive(&tdone[q]);
         // buffer releases, 3 per step by prep: forward step s reads buffers s (L_bb, rb),
         // s-1 (N_b) and s-2 (N2_b); the last forward step stands in for the steps that do
         // not exist; a backward step reads only its own buffer
-        const int own = s % nbuf;
         if (fwd) {
           mbar_arrive(&empty[own]);
           if (s >= 1) mbar_arrive(&empty[(s - 1) % nbuf]);
@@ -438,51 +475,45 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
           mbar_arrive(&empty[own]);
         }
       }
-      double mr[16];
-      {
-        const double* m = slot + i * kLinvLd;
-#pragma unroll
-        for (int kk = 0; kk < 16; kk += 2) {
-          const double2 t2 = *reinterpret_cast<const double2*>(m + kk);
-          mr[kk] = t2.x;
-          mr[kk + 1] = t2.y;
-        }
-      }
-      double* tq = tbuf + (s % kSweepNY) * 16 * R;
-#pragma unroll
-      for (int rr = 0; rr < RL; ++rr) {
-        double a4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(mr[kk], cv[kk * R + rhs_of(rr)], a4[kk & 3]);
-        if (store) tq[i * R + rhs_of(rr)] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-      }
-      __syncwarp();
-      stamp(s, 7);
-      if (lane == 0) mbar_arrive(&tdone[s % kSweepNY]);
     }
     return;
   }
 
   if (warp > kSweepPrepWarps) {
     // ------------------------------------ far -------------------------------------
-    // No barrier among the far warps: a forward row is always updated by the same thread
-    // (row r by thread r mod 96), a backward partial has a fixed slot; each warp arrives
-    // on fardone and on the buffer's empty barrier when its part of the step is done.
-    const int ft = threadIdx.x - 32 * (1 + kSweepPrepWarps);  // 0 .. kSweepFarThreads-1
+    // R <= 2 (kScalar): thread-per-row / thread-per-(column, chunk) FMA loops -- forward: row
+    // r always by thread r mod 96 (no race between steps); backward: 6 row chunks per column,
+    // partials to fpart[s & 3][chunk].  R >= 4: the far work is a skinny GEMM on the FP64
+    // tensor path (mma.sync m8n8k4 f64, SASS DMMA), where the right-hand sides fill the
+    // n-dimension: A = the block's 16 columns of L below block b+1 (rows c0+48 .. c0+15+kd),
+    // the right-hand sides the N = 8 columns of B (R <= 8; two n-tiles for R = 16), zeros
+    // elsewhere.  Fragments: A lane (gr, gc) = A[gr][gc], B lane (gr, gc) = B[gc][gr], C lane
+    // (gr, gc) = C[gr][2gc], C[gr][2gc+1].
+    //   forward   acc[rows] -= L(rows, block b) y_b: 8-row m-tiles on absolute row indices,
+    //             tile T owned by far warp T mod 3, row 8T+gr by lane gr: a row is always
+    //             updated by the same thread, so successive steps never race (no barrier)
+    //   backward  f_b = L(rows, block b)^T x: 4-row k-steps dealt round robin to the far
+    //             warps, each warp's 16 x R partial to fpart[s & 3][warp]; prep adds the three
+    //             partials in a fixed order
+    // Each warp arrives on fardone and on the buffer's empty barrier when its part is done.
+    const int fw = warp - (1 + kSweepPrepWarps);  // 0 .. kSweepFarWarps-1
+    const int ft = threadIdx.x - 32 * (1 + kSweepPrepWarps);
+    const int gr = lane >> 2, gc = lane & 3;
+    constexpr int NT = R > 8 ? 2 : 1;  // n-tiles of 8 right-hand sides
+    constexpr int kFarThreads = 32 * kSweepFarWarps, kFarChunks = kFarThreads / 16;
     for (int s = 0; s < nsteps; ++s) {
       const int b = block_of(s), c0 = 16 * b;
       const double* blk = Lbuf(s);
       if (s < nblk) {
-        // forward: acc_r -= sum_c L(r, c0+c) y_c for rows r in [c0+48, min(n-1, c0+15+kd)]
-        // (block b+2's rows are prep's: they get y_b's term in t_{b+2})
         mbar_wait(&ydone[s % kSweepNY], (unsigned)(s / kSweepNY) & 1u);
         full_wait(s);
-        if (ft == 0) stamp(s, 3);
+        if (fw == 0 && lane == 0) stamp(s, 3);
+        if constexpr (kScalar) {
         const double* y = ych + (s % kSweepNY) * 16 * R;
         const int lo = c0 + 48, hi = min(n - 1, c0 + 15 + kd);
         if (lo <= hi) {
-          int r = lo + ((ft - lo) % kSweepFarThreads + kSweepFarThreads) % kSweepFarThreads;
-          for (; r <= hi; r += kSweepFarThreads) {
+          int r = lo + ((ft - lo) % kFarThreads + kFarThreads) % kFarThreads;
+          for (; r <= hi; r += kFarThreads) {
             const int o = r - c0;  // row offset within the block's columns
             double l[16];          // the row's 16 entries first: one shared-memory latency
             if (o <= kd) {         // every column of the block reaches row r
@@ -497,33 +528,69 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
               }
             }
             double* dst = ring + (size_t)(r % nx) * R;
-            if (R == 1) {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
               double a4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-              for (int c = 0; c < 16; ++c) a4[c & 3] = fma(l[c], y[c], a4[c & 3]);
-              dst[0] -= (a4[0] + a4[1]) + (a4[2] + a4[3]);
-            } else {
-              double acc[R];
-#pragma unroll
-              for (int rr = 0; rr < R; ++rr) acc[rr] = 0.0;
-#pragma unroll
-              for (int c = 0; c < 16; ++c)
-#pragma unroll
-                for (int rr = 0; rr < R; ++rr) acc[rr] = fma(l[c], y[c * R + rr], acc[rr]);
-#pragma unroll
-              for (int rr = 0; rr < R; ++rr) dst[rr] -= acc[rr];
+              for (int c = 0; c < 16; ++c) a4[c & 3] = fma(l[c], y[c * R + rr], a4[c & 3]);
+              dst[rr] -= (a4[0] + a4[1]) + (a4[2] + a4[3]);
             }
           }
         }
+        } else {
+        const double* y = ych + (s % kSweepNY) * 16 * R;
+        const int lo = c0 + 48, hi = min(n - 1, c0 + 15 + kd);
+        if (lo <= hi) {
+          // B fragments (y_b, k = 4 ks + gc, n = gr) for the four k-steps
+          double bf[4][NT];
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const int rh = 8 * nt + gr;
+              bf[ks][nt] = rh < R ? y[(4 * ks + gc) * R + (rh < R ? rh : 0)] : 0.0;
+            }
+          const int t_lo = lo >> 3, t_hi = hi >> 3;
+          int t = t_lo + ((fw - t_lo) % kSweepFarWarps + kSweepFarWarps) % kSweepFarWarps;
+          for (; t <= t_hi; t += kSweepFarWarps) {
+            const int row = 8 * t + gr;                 // this lane's A row
+            const bool rin = row >= lo && row <= hi;
+            double acc[NT][2];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const int k = 4 * ks + gc, o = row - c0 - k;  // L(row, c0 + k)
+              const bool in = rin && o <= kd;
+              const double av = blk[k * ldab + (in ? o : 0)];
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt][0], acc[nt][1], in ? av : 0.0, bf[ks][nt]);
+            }
+            // C[gr][2gc + e] (row 8t + gr, rhs 8 nt + 2 gc + e) -> the accumulator ring
+            const int crow = 8 * t + gr;
+            if (crow >= lo && crow <= hi) {
+              double* dst = ring + (size_t)(crow % nx) * R;
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int rh = 8 * nt + 2 * gc + e;
+                  if (rh < R) dst[rh] -= acc[nt][e];
+                }
+            }
+          }
+        }
+        }
       } else {
-        // backward: f_b(c) = sum over rows r in [c0+48, min(n-1, c0+c+kd)] of L(r, c0+c) x_r
-        // (block b+2's rows are prep's); thread (column ft % 16, chunk ft / 16) takes rows
-        // c0+48+chunk, +6, ... (loads first, four at a time) into its slot of fpart[s & 3]
         if (b + 3 <= nblk - 1) mbar_wait(&ydone[(s - 3) % kSweepNY], (unsigned)((s - 3) / kSweepNY) & 1u);
         full_wait(s);
-        if (ft == 0) stamp(s, 3);
-        constexpr int Q = kSweepFarChunks;
-        const int c = ft & 15, qc = ft >> 4;
+        if (fw == 0 && lane == 0) stamp(s, 3);
+        if constexpr (kScalar) {
+        constexpr int Q = kFarChunks;
+        // thread (column ft / 6, chunk ft % 6) takes rows c0+48+chunk, +6, ... (loads first,
+        // four at a time); consecutive lanes read consecutive rows of one column (contiguous
+        // shared-memory addresses); its partial goes to fpart[s & 3][chunk][column]
+        const int c = ft / Q, qc = ft - (ft / Q) * Q;
         const int hi = c0 + c < n ? min(n - 1, c0 + c + kd) : c0;  // (no rows for columns past n)
         double acc[R][2];
 #pragma unroll
@@ -554,12 +621,52 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
           sl += Q;
           sl = sl >= nx ? sl - nx : sl;
         }
-        double* fp = fpart + (size_t)((s & 3) * kSweepFarThreads + ft) * R;
+        double* fp = fpart + (size_t)(((s & 3) * kFarParts + qc) * 16 + c) * R;
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) fp[rr] = acc[rr][0] + acc[rr][1];
+        } else {
+        const int lo = c0 + 48, hi = min(n - 1, c0 + 15 + kd);
+        double acc[2][NT][2];  // m-tiles (columns 0-7, 8-15) x n-tiles
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        const int nks = hi >= lo ? (hi - lo + 4) >> 2 : 0;
+        for (int ks = fw; ks < nks; ks += kSweepFarWarps) {
+          const int row = lo + 4 * ks + gc;  // k index of this lane's A / B entries
+          const bool rin = row <= hi;
+          const double* xr = ring + (size_t)((rin ? row : lo) % nx) * R;
+          double bv[NT];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int rh = 8 * nt + gr;
+            const double xv = xr[rh < R ? rh : 0];
+            bv[nt] = (rin && rh < R) ? xv : 0.0;
+          }
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const int c = 8 * mt + gr, o = row - c0 - c;  // A[c][k] = L(row, c0 + c)
+            const bool in = rin && o <= kd && c0 + c < n;
+            const double av = blk[c * ldab + (in ? o : 0)];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], in ? av : 0.0, bv[nt]);
+          }
+        }
+        // this warp's partial: column 8 mt + gr, rhs 8 nt + 2 gc + e
+        double* fp = fpart + (size_t)(((s & 3) * kFarParts + fw) * 16) * R;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int rh = 8 * nt + 2 * gc + e;
+              if (rh < R) fp[(8 * mt + gr) * R + rh] = acc[mt][nt][e];
+            }
+        }
       }
       __syncwarp();
-      if (ft == 0) stamp(s, 4);
+      if (fw == 0 && lane == 0) stamp(s, 4);
       if (lane == 0) {
         mbar_arrive(&fardone[s % kSweepNY]);
         mbar_arrive(&empty[s % nbuf]);
@@ -592,20 +699,33 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
     }
     const bool has_prev = fwd ? b >= 1 : b + 1 < nblk;
     const double* prevo = ych + ((s - 1) & (kSweepNY - 1)) * 16 * R;
+    // the product with the previous block's output needs nothing of this step but M: it runs
+    // before t_b is awaited, so only t_b - dot is left on the serial path
+    double dot[RL];
+#pragma unroll
+    for (int rr = 0; rr < RL; ++rr) {
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (has_prev) {
+        if (R == 1) {
+#pragma unroll
+          for (int kk = 0; kk < 16; kk += 2) {
+            const double2 p2 = *reinterpret_cast<const double2*>(prevo + kk);
+            a4[kk & 3] = fma(mr[kk], p2.x, a4[kk & 3]);
+            a4[(kk + 1) & 3] = fma(mr[kk + 1], p2.y, a4[(kk + 1) & 3]);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(mr[kk], prevo[kk * R + rhs_of(rr)], a4[kk & 3]);
+        }
+      }
+      dot[rr] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    }
     mbar_wait(&tdone[qq.slot], qq.par);
     stamp(s, 1);
     const double* tq = tbuf + qq.slot * 16 * R;
     double o[RL];
 #pragma unroll
-    for (int rr = 0; rr < RL; ++rr) {
-      const int r = rhs_of(rr);
-      double a4[4] = {0.0, 0.0, 0.0, 0.0};
-      if (has_prev) {
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(mr[kk], prevo[kk * R + r], a4[kk & 3]);
-      }
-      o[rr] = i < nb ? tq[i * R + r] - ((a4[0] + a4[1]) + (a4[2] + a4[3])) : 0.0;
-    }
+    for (int rr = 0; rr < RL; ++rr) o[rr] = i < nb ? tq[i * R + rhs_of(rr)] - dot[rr] : 0.0;
     double* yo = ych + qq.slot * 16 * R;
     if (store) {
 #pragma unroll

@@ -257,8 +257,10 @@ def trace_solve(batch=1, nrhs=1):
         u = t[sl]
         out[name] = {"step": med(np.diff(u[:, 0])), "chain_wait": med(u[:, 1] - u[:, 0]),
                      "chain_work": med(u[:, 2] - u[:, 1]), "far_work": med(u[:, 4] - u[:, 3]),
-                     "prep_sub": med(u[:, 6] - u[:, 5]), "prep_t": med(u[:, 7] - u[:, 6]),
-                     "t_ready_before_chain": med(u[:, 1] - u[:, 7])}
+                     "t_waits_after_subst": med(u[:, 6] - u[:, 5]), "t_work": med(u[:, 7] - u[:, 6]),
+                     "chain_wake_after_t": med(u[:, 1] - u[:, 7]),
+                     "t_inputs_after_prev2_chain_end": (med(u[2:, 6] - u[:-2, 2]) if name == "fwd"
+                                                        else med(u[2:, 6] - u[:-2, 2]))}
     out["fwd"]["far_start_after_ydone"] = med(t[4:nblk - 4, 3] - t[4:nblk - 4, 2])
     out["total_cycles"] = float(t[-1, 2] - t[0, 0])
     print(json.dumps(out), flush=True)
