@@ -42,7 +42,12 @@ constexpr int kSweepWarps = 8;
 constexpr int kSweepThreads = 32 * kSweepWarps;
 constexpr int kSweepPrepWarps = 3;
 constexpr int kSweepFarWarps = 3;
-constexpr int kSweepNP = 6;      // prep ring slots
+// prep ring slots and backward far partials per column: the FMA path (R <= 2) runs prep
+// further ahead and splits a column over 6 row chunks; the DMMA path (R >= 8) keeps 4 slots
+// and one partial per far warp, so that two R = 8 CTAs fit on an SM
+__host__ __device__ constexpr int sweep_np(int R) { return R <= 2 ? 6 : 4; }
+__host__ __device__ constexpr int sweep_parts(int R) { return R <= 2 ? 6 : 3; }
+constexpr int kSweepNPMax = 6;
 constexpr int kSweepNY = 4;      // chain-output / t ring slots (a power of two)
 constexpr int kLinvLd = 18;      // row stride of a prep matrix (16-byte aligned rows)
 constexpr int kPrepSlot = 2 * 16 * kLinvLd;  // [0] Linv (for t), [1] H / G (for the chain)
@@ -59,12 +64,32 @@ struct SweepGeom {
 __host__ __device__ inline size_t sweep_smem_doubles(const SweepGeom& g, int R) {
   return (size_t)g.nbuf * 16 * g.ldab          // L ring
          + (size_t)g.nbuf * 16 * R              // right-hand-side rows per buffer
-         + (size_t)kSweepNP * kPrepSlot         // prep ring
+         + (size_t)sweep_np(R) * kPrepSlot      // prep ring
          + (size_t)kSweepNY * 16 * R            // chain outputs
          + (size_t)kSweepNY * 16 * R            // t
-         + (size_t)4 * 2 * kSweepFarWarps * 16 * R  // backward far partials (a ring of 4 steps)
+         + (size_t)4 * sweep_parts(R) * 16 * R  // backward far partials (a ring of 4 steps)
          + (size_t)kSweepPrepWarps * 16 * R     // the prep warps' staged vectors
          + (size_t)g.nx * R;                    // accumulator / solution ring
+}
+
+// C (16 x R) += A (16 x 16, row r at a[r * lda + k]) * B (16 x R, b[k * R + n]) on the FP64
+// tensor path (R = 8 or 16: one or two 8-wide n-tiles; mma.sync m8n8k4 f64).  Lane (gr, gc)
+// ends holding C[8 mt + gr][8 nt + 2 gc + e] in acc[mt][nt][e].
+template <int R>
+__device__ __forceinline__ void dmma_16x16xR(const double* a, int lda, const double* b, double (&acc)[2][R / 8][2]) {
+  const int lane = threadIdx.x & 31, gr = lane >> 2, gc = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    double af[2], bf[R / 8];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) af[mt] = a[(8 * mt + gr) * lda + 4 * ks + gc];
+#pragma unroll
+    for (int nt = 0; nt < R / 8; ++nt) bf[nt] = b[(4 * ks + gc) * R + 8 * nt + gr];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < R / 8; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
+  }
 }
 
 // a phase-tracked position in a ring of `size` slots: slot and parity advance together
@@ -200,11 +225,12 @@ __device__ __forceinline__ void prep_backward(const double* blk, int rows, int n
 }
 
 template <int R>
-__global__ void __launch_bounds__(kSweepThreads, R <= 4 ? 2 : 1)
+__global__ void __launch_bounds__(kSweepThreads, R <= 8 ? 2 : 1)
 pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0, int64_t ldb, int64_t stride_b,
                    int nrhs, int groups, SweepGeom g, int32_t* info, const int32_t* skip, int check_diag) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) unsigned long long full[8], empty[8], pfull[kSweepNP], pempty[kSweepNP];
+  constexpr int kSweepNP = sweep_np(R);
+  __shared__ __align__(8) unsigned long long full[8], empty[8], pfull[kSweepNPMax], pempty[kSweepNPMax];
   __shared__ __align__(8) unsigned long long ydone[kSweepNY], fardone[kSweepNY], tdone[kSweepNY], fwd_done;
 
   const int mat = blockIdx.x / groups, grp = blockIdx.x - mat * groups;
@@ -230,7 +256,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   double* ych = prep + kSweepNP * kPrepSlot;          // [NY][16][R]
   double* tbuf = ych + kSweepNY * 16 * R;             // [NY][16][R]
   double* fpart = tbuf + kSweepNY * 16 * R;           // [4][kFarParts][16][R]
-  double* cstage = fpart + 4 * 2 * kSweepFarWarps * 16 * R;  // [kSweepPrepWarps][16][R]
+  double* cstage = fpart + 4 * sweep_parts(R) * 16 * R;  // [kSweepPrepWarps][16][R]
   double* ring = cstage + kSweepPrepWarps * 16 * R;   // [nx][R]
 
   if (threadIdx.x < 8) {
@@ -273,7 +299,8 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   auto full_wait = [&](int s) { mbar_wait(&full[s % nbuf], (unsigned)(s / nbuf) & 1u); };
   constexpr int RL = R == 1 ? 1 : R / 2;
   constexpr bool kScalar = R <= 2;  // far work on the FMA pipe (else DMMA)
-  constexpr int kFarParts = kScalar ? 2 * kSweepFarWarps : kSweepFarWarps;  // backward partials per column
+  constexpr int kFarParts = sweep_parts(R);  // backward partials per column
+  static_assert(kFarParts == (kScalar ? 2 * kSweepFarWarps : kSweepFarWarps), "partials per column");
   const int i = lane & 15, h = lane >> 4;
   const bool store = R > 1 || h == 0;  // R == 1: both halves compute, only h == 0 stores
   auto rhs_of = [&](int rr) { return R == 1 ? 0 : h + 2 * rr; };
@@ -437,6 +464,22 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
         }
       }
       __syncwarp();
+      if constexpr (R >= 8) {
+        // t = Linv_b cv (16 x R) on the tensor path
+        const int gr = lane >> 2, gc = lane & 3;
+        double acc[2][R / 8][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < R / 8; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        dmma_16x16xR<R>(slot, kLinvLd, cv, acc);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < R / 8; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) tq[(8 * mt + gr) * R + 8 * nt + 2 * gc + e] = acc[mt][nt][e];
+      } else {
 #pragma unroll
       for (int rr = 0; rr < RL; ++rr) {
         double a4[4] = {0.0, 0.0, 0.0, 0.0};
@@ -452,6 +495,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
           for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(mr[kk], cv[kk * R + rhs_of(rr)], a4[kk & 3]);
         }
         if (store) tq[i * R + rhs_of(rr)] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      }
       }
       __syncwarp();
       stamp(s, 7);
@@ -699,51 +743,96 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
     }
     const bool has_prev = fwd ? b >= 1 : b + 1 < nblk;
     const double* prevo = ych + ((s - 1) & (kSweepNY - 1)) * 16 * R;
-    // the product with the previous block's output needs nothing of this step but M: it runs
-    // before t_b is awaited, so only t_b - dot is left on the serial path
-    double dot[RL];
+    if constexpr (R >= 8) {
+      // right-hand sides fill the n-dimension of a DMMA product: C = M . (previous output),
+      // then out = t_b - C; lane (gr, gc) owns rows gr, 8+gr and right-hand sides 2gc, 2gc+1
+      // (+8 for R = 16)
+      constexpr int NT = R / 8;
+      const int gr = lane >> 2, gc = lane & 3;
+      double acc[2][NT][2];
 #pragma unroll
-    for (int rr = 0; rr < RL; ++rr) {
-      double a4[4] = {0.0, 0.0, 0.0, 0.0};
-      if (has_prev) {
-        if (R == 1) {
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int kk = 0; kk < 16; kk += 2) {
-            const double2 p2 = *reinterpret_cast<const double2*>(prevo + kk);
-            a4[kk & 3] = fma(mr[kk], p2.x, a4[kk & 3]);
-            a4[(kk + 1) & 3] = fma(mr[kk + 1], p2.y, a4[(kk + 1) & 3]);
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+      if (has_prev) dmma_16x16xR<R>(prep + pp.slot * kPrepSlot + 16 * kLinvLd, kLinvLd, prevo, acc);
+      mbar_wait(&tdone[qq.slot], qq.par);
+      stamp(s, 1);
+      const double* tq = tbuf + qq.slot * 16 * R;
+      double* yo = ych + qq.slot * 16 * R;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = 8 * mt + gr, rh = 8 * nt + 2 * gc + e;
+            const double o = row < nb ? tq[row * R + rh] - acc[mt][nt][e] : 0.0;
+            acc[mt][nt][e] = o;
+            yo[row * R + rh] = o;
+            if (!fwd) ring[(size_t)(xs + row) * R + rh] = o;  // for the far dot products
           }
-        } else {
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(mr[kk], prevo[kk * R + rhs_of(rr)], a4[kk & 3]);
-        }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&ydone[qq.slot]);
+        mbar_arrive(&pempty[pp.slot]);
       }
-      dot[rr] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-    }
-    mbar_wait(&tdone[qq.slot], qq.par);
-    stamp(s, 1);
-    const double* tq = tbuf + qq.slot * 16 * R;
-    double o[RL];
-#pragma unroll
-    for (int rr = 0; rr < RL; ++rr) o[rr] = i < nb ? tq[i * R + rhs_of(rr)] - dot[rr] : 0.0;
-    double* yo = ych + qq.slot * 16 * R;
-    if (store) {
-#pragma unroll
-      for (int rr = 0; rr < RL; ++rr) {
-        yo[i * R + rhs_of(rr)] = o[rr];
-        if (!fwd) ring[(size_t)(xs + i) * R + rhs_of(rr)] = o[rr];  // for the far dot products
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&ydone[qq.slot]);
-      mbar_arrive(&pempty[pp.slot]);
-    }
-    if (store) {  // to global memory after the signals (nothing in this CTA waits on it soon)
       double* brow = bm + c0;
 #pragma unroll
-      for (int rr = 0; rr < RL; ++rr)
-        if (i < nb && rhs_of(rr) < rv) brow[(int64_t)rhs_of(rr) * ldb + i] = o[rr];
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = 8 * mt + gr, rh = 8 * nt + 2 * gc + e;
+            if (row < nb && rh < rv) brow[(int64_t)rh * ldb + row] = acc[mt][nt][e];
+          }
+    } else {
+    // the product with the previous block's output needs nothing of this step but M: it runs
+      // before t_b is awaited, so only t_b - dot is left on the serial path
+      double dot[RL];
+  #pragma unroll
+      for (int rr = 0; rr < RL; ++rr) {
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        if (has_prev) {
+          if (R == 1) {
+  #pragma unroll
+            for (int kk = 0; kk < 16; kk += 2) {
+              const double2 p2 = *reinterpret_cast<const double2*>(prevo + kk);
+              a4[kk & 3] = fma(mr[kk], p2.x, a4[kk & 3]);
+              a4[(kk + 1) & 3] = fma(mr[kk + 1], p2.y, a4[(kk + 1) & 3]);
+            }
+          } else {
+  #pragma unroll
+            for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(mr[kk], prevo[kk * R + rhs_of(rr)], a4[kk & 3]);
+          }
+        }
+        dot[rr] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      }
+      mbar_wait(&tdone[qq.slot], qq.par);
+      stamp(s, 1);
+      const double* tq = tbuf + qq.slot * 16 * R;
+      double o[RL];
+  #pragma unroll
+      for (int rr = 0; rr < RL; ++rr) o[rr] = i < nb ? tq[i * R + rhs_of(rr)] - dot[rr] : 0.0;
+      double* yo = ych + qq.slot * 16 * R;
+      if (store) {
+  #pragma unroll
+        for (int rr = 0; rr < RL; ++rr) {
+          yo[i * R + rhs_of(rr)] = o[rr];
+          if (!fwd) ring[(size_t)(xs + i) * R + rhs_of(rr)] = o[rr];  // for the far dot products
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&ydone[qq.slot]);
+        mbar_arrive(&pempty[pp.slot]);
+      }
+      if (store) {  // to global memory after the signals (nothing in this CTA waits on it soon)
+        double* brow = bm + c0;
+  #pragma unroll
+        for (int rr = 0; rr < RL; ++rr)
+          if (i < nb && rhs_of(rr) < rv) brow[(int64_t)rhs_of(rr) * ldb + i] = o[rr];
+      }
     }
     stamp(s, 2);
     if (s == nblk - 1) {

@@ -175,7 +175,9 @@ static bcg::SweepGeom sweep_geom(int n, int kd, int ldab, int R) {
   return g;
 }
 
-static int sweep_r(int64_t nrhs) { return nrhs <= 1 ? 1 : nrhs <= 2 ? 2 : nrhs <= 4 ? 4 : nrhs <= 8 ? 8 : 16; }
+// right-hand sides per CTA: 1 and 2 on the FMA path; 3..8 one 8-wide DMMA n-tile (measured
+// faster for 4 than the FMA path), more: 16 per CTA (two n-tiles)
+static int sweep_r(int64_t nrhs) { return nrhs <= 1 ? 1 : nrhs <= 2 ? 2 : nrhs <= 8 ? 8 : 16; }
 
 template <int R>
 static int launch_sweep_t(const double* ab, int64_t sab, double* b, int64_t ldb, int64_t sb, int nrhs, int batch,
@@ -201,7 +203,6 @@ static int launch_solve(const double* ab, int64_t sab, double* b, int64_t ldb, i
     switch (R) {
       case 1: return launch_sweep_t<1>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
       case 2: return launch_sweep_t<2>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
-      case 4: return launch_sweep_t<4>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
       case 8: return launch_sweep_t<8>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
       default: return launch_sweep_t<16>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
     }
