@@ -3,8 +3,10 @@
 // Entry points replace the reference's factorization engines and solve:
 //   bcg_dpbtrf / bcg_dpbtrf_batched  <- factor_blocked_serial (pkg/src/bandchol/blocked.py:363-385),
 //                                       factor_blocked_parallel (pkg/src/bandchol/parallel.py:130-166)
-//   bcg_dpbtrs / bcg_dpbtrs_batched  <- solve_with_factor (pkg/src/bandchol/core.py:216-240)
-//   bcg_dpbsv_batched                <- factor + solve of config C5 fused in one launch
+//   bcg_dpbtrs / bcg_dpbtrs_batched(_nrhs)  <- solve_with_factor (pkg/src/bandchol/core.py:216-240),
+//                                       up to 16 right-hand sides per pass over L
+//   bcg_dpbsv_batched                <- factor + solve of config C5: the batched factorization
+//                                       kernel, then the streamed solve kernel
 #include <climits>
 #include <cstdarg>
 #include <cstdio>

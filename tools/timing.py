@@ -198,40 +198,6 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_cta":
     trace_cta("C5", 296)
 
 
-def trace_bwd(batch=1):
-    """Backward-sweep phase breakdown of the fused dpbsv kernel (block 0, matrix 0)."""
-    from paper_2305_04635_b200 import _lib
-    n, k = 4096, 100
-    a = np.stack([generate_spd(n, k, s).data for s in range(min(batch, 8))])
-    a = np.concatenate([a] * ((batch + 7) // 8))[:batch]
-    b = np.stack([make_rhs(n, s) for s in range(batch)])
-    a0, b0 = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
-    nblk = n // 16
-    buf = torch.zeros(1 + 8 * (2 * nblk + 4), dtype=torch.int64, device="cuda")
-    lib = _lib.load()
-    lib.bcg_set_trace(buf.data_ptr(), buf.numel() * 8)
-    w, wb = a0.clone(), b0.clone()
-    bc.dpbsv_batched_device(w, n, k, k + 1, wb, batch)
-    torch.cuda.synchronize()
-    lib.bcg_set_trace(None, 0)
-    t = buf.cpu().numpy()[1:].reshape(-1, 8).astype(np.float64)
-    f = t[:nblk]
-    bw = t[nblk + 1: 2 * nblk + 1]
-    med = lambda x: float(np.median(x))  # noqa: E731
-    out = {"batch": batch, "factor_step": med(np.diff(f[:-2, 0])),
-           "bwd_wait": med(bw[:, 1] - bw[:, 0]), "bwd_warp0": med(bw[1:-1, 2] - bw[1:-1, 1]),
-           "bwd_invert": med(bw[1:-1, 4] - bw[1:-1, 1]), "bwd_far": med(bw[1:-1, 5] - bw[1:-1, 1]),
-           "bwd_sync": med(bw[:, 3] - bw[:, 1]),
-           "bwd_block": med(bw[:-1, 0] - bw[1:, 0]),
-           "bwd_total_cycles": float(bw[0, 3] - bw[-1, 0]), "factor_total_cycles": float(f[-3, 0] - f[0, 0])}
-    print(json.dumps(out), flush=True)
-
-
-if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "trace_bwd":
-    trace_bwd(1)
-    trace_bwd(296)
-
-
 def trace_solve(batch=1, nrhs=1):
     """Per-step phase breakdown of the streamed solve (band_sweep.cuh, CTA 0), SM cycles."""
     from paper_2305_04635_b200 import _lib
