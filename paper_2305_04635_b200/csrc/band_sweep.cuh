@@ -304,6 +304,8 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   const int i = lane & 15, h = lane >> 4;
   const bool store = R > 1 || h == 0;  // R == 1: both halves compute, only h == 0 stores
   auto rhs_of = [&](int rr) { return R == 1 ? 0 : h + 2 * rr; };
+  // prep's t staging (R >= 8: contiguous runs, lane half h takes rhs [RL h, RL h + RL))
+  auto stage_of = [&](int rr) { return R >= 8 ? RL * h + rr : rhs_of(rr); };
 
   if (warp == kSweepWarps - 1) {
     // ---------------------------------- producer ----------------------------------
@@ -432,7 +434,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
         for (int rr = 0; rr < RL; ++rr) {
           double a4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(l[kk], v2[kk * R + rhs_of(rr)], a4[kk & 3]);
+          for (int kk = 0; kk < 16; ++kk) a4[kk & 3] = fma(l[kk], v2[kk * R + stage_of(rr)], a4[kk & 3]);
           u2[rr] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         }
       }
@@ -443,7 +445,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
         if (store) {
 #pragma unroll
           for (int rr = 0; rr < RL; ++rr) {
-            const int r = rhs_of(rr);
+            const int r = stage_of(rr);
             cv[i * R + r] = (rb[i * R + r] + acc[r]) - u2[rr];
             acc[r] = 0.0;  // the slot's next row starts from zero
           }
@@ -455,7 +457,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
         if (store) {
 #pragma unroll
           for (int rr = 0; rr < RL; ++rr) {
-            const int r = rhs_of(rr);
+            const int r = stage_of(rr);
             double f = 0.0;
 #pragma unroll
             for (int w = 0; w < kFarParts; ++w) f += fp[(size_t)(w * 16 + i) * R + r];
