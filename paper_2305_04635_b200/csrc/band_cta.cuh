@@ -120,7 +120,7 @@ __device__ __forceinline__ void trace_stamp_to(unsigned long long* tr, int j, in
   if (tr) {
     const unsigned long long idx = 1 + (unsigned long long)j * kTracePhases + phase;
     if (idx < g_trace_cap) tr[idx] = gtime();
-    if (phase == 0 && (unsigned long long)j + 1 > tr[0]) tr[0] = j + 1;
+    if (phase == 0) tr[0] = j + 1;  // (steps are stamped in increasing order: no read-back)
   }
 }
 

@@ -547,18 +547,20 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
     const int gr = lane >> 2, gc = lane & 3;
     constexpr int NT = R > 8 ? 2 : 1;  // n-tiles of 8 right-hand sides
     constexpr int kFarThreads = 32 * kSweepFarWarps, kFarChunks = kFarThreads / 16;
-    for (int s = 0; s < nsteps; ++s) {
+    RingPos kb;  // this step's L buffer and its full-phase parity (no divisions in the loop)
+    for (int s = 0; s < nsteps; ++s, kb.next(nbuf)) {
       const int b = block_of(s), c0 = 16 * b;
-      const double* blk = Lbuf(s);
+      const double* blk = Lring + (size_t)kb.slot * 16 * ldab;
       if (s < nblk) {
         mbar_wait(&ydone[s % kSweepNY], (unsigned)(s / kSweepNY) & 1u);
-        full_wait(s);
+        mbar_wait(&full[kb.slot], kb.par);
         if (fw == 0 && lane == 0) stamp(s, 3);
         if constexpr (kScalar) {
         const double* y = ych + (s % kSweepNY) * 16 * R;
         const int lo = c0 + 48, hi = min(n - 1, c0 + 15 + kd);
         if (lo <= hi) {
           int r = lo + ((ft - lo) % kFarThreads + kFarThreads) % kFarThreads;
+          int sl = r % nx;  // ring slot of row r, advanced without divisions
           for (; r <= hi; r += kFarThreads) {
             const int o = r - c0;  // row offset within the block's columns
             double l[16];          // the row's 16 entries first: one shared-memory latency
@@ -573,7 +575,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
                 l[c] = in ? lv : 0.0;
               }
             }
-            double* dst = ring + (size_t)(r % nx) * R;
+            double* dst = ring + (size_t)sl * R;
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
               double a4[4] = {0.0, 0.0, 0.0, 0.0};
@@ -581,6 +583,8 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
               for (int c = 0; c < 16; ++c) a4[c & 3] = fma(l[c], y[c * R + rr], a4[c & 3]);
               dst[rr] -= (a4[0] + a4[1]) + (a4[2] + a4[3]);
             }
+            sl += kFarThreads;
+            while (sl >= nx) sl -= nx;
           }
         }
         } else {
@@ -629,7 +633,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
         }
       } else {
         if (b + 3 <= nblk - 1) mbar_wait(&ydone[(s - 3) % kSweepNY], (unsigned)((s - 3) / kSweepNY) & 1u);
-        full_wait(s);
+        mbar_wait(&full[kb.slot], kb.par);
         if (fw == 0 && lane == 0) stamp(s, 3);
         if constexpr (kScalar) {
         constexpr int Q = kFarChunks;
@@ -715,7 +719,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
       if (fw == 0 && lane == 0) stamp(s, 4);
       if (lane == 0) {
         mbar_arrive(&fardone[s % kSweepNY]);
-        mbar_arrive(&empty[s % nbuf]);
+        mbar_arrive(&empty[kb.slot]);
       }
     }
     return;
