@@ -58,11 +58,12 @@ struct MultiGeom {
 };
 
 // ---- workspace ---------------------------------------------------------------------
-// [ctrl: 8 ints][tcnt: nblk*(T+1)][lrdy: nblk*(T+1)]
+// [ctrl: 8 ints][tcnt: nblk*(T+1)][lrdy: nblk*(T+1)] (zeroed per launch) [inv: nblk*NB*NB doubles]
 struct MultiWs {
   int* ctrl;  // [0] ticket, [1] fail (global column + 1), [2] pivot's SM id + 1
   int* tcnt;
   int* lrdy;
+  double* inv;  // inv[j][k*NB + c] = (L(j,j)^-1)(c, k): the row tasks' TRSM is a product with it
 };
 
 __host__ __device__ inline size_t multi_flag_bytes(int nblk, int T) {
@@ -76,6 +77,7 @@ __host__ __device__ inline MultiWs multi_ws(void* base, int nblk, int T) {
   w.ctrl = p;
   w.tcnt = p + 8;
   w.lrdy = w.tcnt + (size_t)nblk * (T + 1);
+  w.inv = (double*)((char*)base + multi_flag_bytes(nblk, T));
   return w;
 }
 
@@ -160,7 +162,14 @@ __device__ __forceinline__ void store_tile(const double* s, double* ab, const Mu
 // kSub: C -= A B^T (C read from sC)      else: C = A B^T.  NW warps (warp index wg within
 // the group, synchronised by named barrier bar_id over bar_cnt threads), M = N = K = NB.
 // A(m,k) = sA[k*LD + m], B(n,k) = sB[k*LD + n], C(m,n) = sC[n*LD + m].  sC must not alias sA/sB.
-template <int NB, bool kSub, int NW = 8>
+// kBTri: B(n,k) = 0 for k > n (the transposed inverse of a lower-triangular block): k-steps
+// past an 8-column block's last column are skipped.
+__device__ __forceinline__ void dmma884p(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+template <int NB, bool kSub, int NW = 8, bool kBTri = false>
 __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const double* sB, int wg = threadIdx.x >> 5,
                                           int bar_id = 0, int bar_cnt = kMultiThreads) {
   constexpr int LD = MultiTile<NB>::LD;
@@ -181,7 +190,7 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
       acc[tm][tn][0] = kSub ? sC[nn * LD + m] : 0.0;
       acc[tm][tn][1] = kSub ? sC[(nn + 1) * LD + m] : 0.0;
     }
-#pragma unroll 4
+#pragma unroll
   for (int k0 = 0; k0 < NB; k0 += 4) {
     double a[TM], b[TN];
 #pragma unroll
@@ -194,7 +203,10 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
 #pragma unroll
     for (int tm = 0; tm < TM; ++tm)
 #pragma unroll
-      for (int tn = 0; tn < TN; ++tn) dmma884(acc[tm][tn][0], acc[tm][tn][1], a[tm], b[tn]);
+      for (int tn = 0; tn < TN; ++tn) {
+        if (kBTri && WN == 1 && k0 > tn * 8 + 7) continue;  // (WN == 1: the block index is static)
+        dmma884p(acc[tm][tn][0], acc[tm][tn][1], a[tm], b[tn]);
+      }
   }
   named_sync(bar_id, bar_cnt);  // sC may be read by other warps' fragment loads above (kSub)
 #pragma unroll
@@ -217,8 +229,12 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
 // diagonal become don't-care.  Rows past nvalid are identity rows.  Failure: after a bad
 // pivot every later pivot is NaN, so the failing column is the first lane whose L(r, r)
 // is not > 0.  Returns it or -1 (uniform).
-__device__ __forceinline__ int warp_potrf32(double* s, int ld, int nvalid, double* lbuf) {
-  (void)lbuf;
+//
+// For the inverse warp (warp_inverse32) trailing this one column group by column group:
+// sdinv[c] = 1 / L(c, c), and colbar[c / 4] (one mbarrier per four columns, one arrival,
+// one phase per call) is completed once columns 4(c/4)..4(c/4)+3 and their sdinv are written.
+__device__ __forceinline__ int warp_potrf32(double* s, int ld, int nvalid, double* sdinv,
+                                            unsigned long long* colbar) {
   const int r = threadIdx.x & 31;
   double row[32];
   if (nvalid == 32) {
@@ -251,7 +267,9 @@ __device__ __forceinline__ int warp_potrf32(double* s, int ld, int nvalid, doubl
     row[c] = lrc;
     double* sc = s + c * ld;
     sc[r] = lrc;
+    if (r == 0) sdinv[c] = rs;
     __syncwarp();
+    if ((c & 3) == 3 && r == 0) mbar_arrive(colbar + (c >> 2));  // (release: cumulative over the warp barrier)
 #pragma unroll
     for (int h = 0; h < 16; ++h) {
       if (2 * h + 1 >= c + 2) {
@@ -269,6 +287,54 @@ __device__ __forceinline__ int warp_potrf32(double* s, int ld, int nvalid, doubl
   const unsigned bad = __ballot_sync(kFull, !(dgl > 0.0));
   __syncwarp();
   return bad ? __ffs(bad) - 1 : -1;
+}
+
+// ---- L^-1 of the 32x32 block, one warp, in lock step behind warp_potrf32 ------------------
+// Lane k applies the POTRF's column operations to e_k: y[c] = (y[c] - sum_{c'<c} y[c'] L(c,c')) / L(c,c),
+// i.e. y = e_k^T L^-T, so y[c] = (L^-1)(c, k).  Stored as sInv[k*LD + c]: the B operand of
+// X = A L^-T = A (L^-1)^T in tile_gemm's convention (B(n, k) = sB[k*LD + n]).  Column c of L
+// and sdinv[c] are read from the tile the POTRF warp is writing, four columns behind it.
+__device__ __forceinline__ void warp_inverse32(const double* s, int ld, const double* sdinv, double* sInv,
+                                               unsigned long long* colbar, unsigned parity) {
+  const int k = threadIdx.x & 31;
+  double v[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) v[c] = (c == k) ? 1.0 : 0.0;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    if ((c & 3) == 0) mbar_wait(colbar + (c >> 2), parity);
+    const double y = v[c] * sdinv[c];
+    sInv[k * ld + c] = y;
+    const double* sc = s + c * ld;
+#pragma unroll
+    for (int h = 0; h < 16; ++h) {
+      if (2 * h + 1 >= c + 1) {
+        const double2 l2 = reinterpret_cast<const double2*>(sc)[h];
+        if (2 * h >= c + 1) v[2 * h] = fma(-y, l2.x, v[2 * h]);
+        v[2 * h + 1] = fma(-y, l2.y, v[2 * h + 1]);
+      }
+    }
+  }
+}
+
+// dense NB x NB block (ld NB) in global memory <-> smem tile; every load before the first store
+template <int NB, int NT>
+__device__ __forceinline__ void load_dense(double* s, const double* src, int t) {
+  constexpr int LD = MultiTile<NB>::LD;
+  constexpr int E = NB * NB / NT;
+  double v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = __ldcg(src + t + e * NT);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int idx = t + e * NT;
+    s[(idx / NB) * LD + (idx % NB)] = v[e];
+  }
+}
+template <int NB, int NT>
+__device__ __forceinline__ void store_dense(const double* s, double* dst, int t) {
+  constexpr int LD = MultiTile<NB>::LD;
+  for (int idx = t; idx < NB * NB; idx += NT) __stcg(dst + idx, s[(idx / NB) * LD + (idx % NB)]);
 }
 
 // ---- TRSM of a tile by substitution: X <- X L^-T (L lower NB x NB), row per thread ------
@@ -300,63 +366,97 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   constexpr int LD = MultiTile<NB>::LD;
   __shared__ int s_ok;
   __shared__ int s_fail;
-  __shared__ double lbuf[32];
   __shared__ double sdinv[NB];
   const int T = g.T, nblk = g.nblk;
   const int warp = warp_uniform(threadIdx.x >> 5);  // provably warp-uniform branches
   auto TC = [&](int R, int d) -> int* { return ws.tcnt + (size_t)R * (T + 1) + d; };
   auto LR = [&](int R, int d) -> int* { return ws.lrdy + (size_t)R * (T + 1) + d; };
-  auto make_dinv = [&](const double* sL) {  // 1/diag for the substitution TRSM
-    if (threadIdx.x < NB) sdinv[threadIdx.x] = 1.0 / sL[threadIdx.x * LD + threadIdx.x];
-  };
 
   unsigned smid;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   if (blockIdx.x == 0) {
     if (threadIdx.x == 0) st_release(ws.ctrl + 2, (int)smid + 1);
     // ------------------------------ pivot ---------------------------------------
-    double* sD = smem;           // current diagonal tile (fully updated)
-    double* sLp = smem + E;      // L(j, j-1) from the previous step
-    double* f0 = smem + 2 * E;   // free tiles
-    double* f1 = smem + 3 * E;
-    double* f2 = smem + 4 * E;
+    // Warp roles (warp w sits on SM sub-partition w & 3):
+    //   0      POTRF of (j,j)                       -- the chain, alone on SMSP 0 in stage A
+    //   1      L(j,j)^-1 in lock step behind it
+    //   2,3    lookback A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T     } stage A, as soon as the
+    //   6,7    lookback A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T   } tiles have landed
+    //   4-7    service: flag waits, tile loads, write-backs and publishes
+    // Stage B (after the POTRF): warps 0-3 run the TRSM as a product with L(j,j)^-1 and the
+    // SYRK of (j+1,j+1); warps 4-7 write back and publish L(j,j), its inverse and L(j+1,j)
+    // beside them.  On the chain per step: POTRF, two 32^3 tile products, three barriers.
+    __shared__ __align__(8) unsigned long long colbar[8];
+    double* sD = smem;            // current diagonal tile (fully updated)
+    double* sLp = smem + E;       // L(j, j-1) from the previous step
+    double* sInv = smem + 2 * E;  // L(j,j)^-1, sInv[k*LD + c] = Linv(c, k)
+    double* f0 = smem + 3 * E;    // free tiles
+    double* f1 = smem + 4 * E;
+    double* f2 = smem + 5 * E;
+    double* f3 = smem + 6 * E;
     unsigned long long* tr = g_trace;
     load_tile<NB, kMultiThreads>(sD, ab, g, 0, 0, threadIdx.x);
-    if (threadIdx.x == 0) s_fail = -1;
+    if (threadIdx.x == 0) {
+      s_fail = -1;
+      s_ok = 1;
+      for (int i = 0; i < 8; ++i) mbar_init(colbar + i, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     int fail_col = -1;
     for (int j = 0; j < nblk; ++j) {
       const int nvalid = min(NB, g.n - j * NB);
       double* sW = f0;   // L(j+1, j-1)
-      double* sP = f1;   // A(j+1, j) -> L(j+1, j)
+      double* sP = f1;   // A(j+1, j)
       double* sD2 = f2;  // A(j+1, j+1)
+      double* sX = f3;   // L(j+1, j)
       const bool next = j + 1 < nblk;
       const bool has_w = next && (j >= 1) && (T >= 2);
       if (threadIdx.x == 0) trace_stamp_to(tr, j, 0);
-      // ---- stage A: warp 0 factors (j,j) || warps 1-7 fetch the next step's tiles ----
+      // ---- stage A ----
       if (warp == 0) {
-        const int f = warp_potrf32(sD, LD, nvalid, lbuf);
-        if (threadIdx.x == 0) s_fail = f;
-      } else if (next) {
-        const int lo = max(0, j + 1 - T);
-        const int need = max(0, j - 1 - lo);  // worker updates m in [lo, j-2]
-        if (threadIdx.x == 32) {
-          bool ok = spin_ge(TC(j + 1, 1), need, ws.ctrl + 1, 64) && spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
-          trace_stamp_to(tr, j, 6);
-          if (ok && has_w) ok = spin_ge(LR(j + 1, 2), 1, ws.ctrl + 1, 64);
-          trace_stamp_to(tr, j, 7);
-          s_ok = ok;
+        const int f = warp_potrf32(sD, LD, nvalid, sdinv, colbar);
+        if (threadIdx.x == 0) {
+          s_fail = f;
+          trace_stamp_to(tr, j, 1);
         }
-        named_sync(1, 224);
-        if (warp_uniform(s_ok)) {
-          const int t = threadIdx.x - 32;
-          load_tile<NB, 224>(sP, ab, g, j + 1, j, t);
-          load_tile<NB, 224>(sD2, ab, g, j + 1, j + 1, t);
-          if (has_w) load_tile<NB, 224>(sW, ab, g, j + 1, j - 1, t);
+      } else if (warp == 1) {
+        warp_inverse32(sD, LD, sdinv, sInv, colbar, (unsigned)(j & 1));
+      } else if (next) {
+        if (warp >= 4) {
+          const int t = threadIdx.x - 128;
+          const int lo = max(0, j + 1 - T);
+          const int need = max(0, j - 1 - lo);  // worker updates m in [lo, j-2]
+          if (t == 0) {
+            bool ok = spin_ge(TC(j + 1, 1), need, ws.ctrl + 1, 64) && spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
+            s_ok = ok;
+          }
+          named_sync(3, 128);
+          if (warp_uniform(s_ok)) {
+            load_tile<NB, 128>(sP, ab, g, j + 1, j, t);
+            load_tile<NB, 128>(sD2, ab, g, j + 1, j + 1, t);
+          }
+          if (has_w) {
+            if (t == 0 && s_ok) {
+              s_ok = spin_ge(LR(j + 1, 2), 1, ws.ctrl + 1, 64);
+              trace_stamp_to(tr, j, 6);
+            }
+            named_sync(3, 128);
+            if (warp_uniform(s_ok)) load_tile<NB, 128>(sW, ab, g, j + 1, j - 1, t);
+          }
+        }
+        named_sync(5, 192);  // warps 2-7: the tiles are in shared memory
+        if (has_w && warp_uniform(s_ok)) {
+          if (warp == 2 || warp == 3) {
+            tile_gemm<NB, true, 2>(sP, sW, sLp, warp - 2, 6, 64);  // A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T
+            if (threadIdx.x == 64) trace_stamp_to(tr, j, 7);
+          } else if (warp >= 6) {
+            tile_gemm<NB, true, 2>(sD2, sW, sW, warp - 6, 7, 64);  // A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
+          }
         }
       }
       __syncthreads();
-      if (threadIdx.x == 0) trace_stamp_to(tr, j, 1);
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 2);
       const int fl = warp_uniform(s_fail);
       const int okn = warp_uniform(s_ok);
       if (fl >= 0) {
@@ -365,36 +465,42 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         break;
       }
       if (next && !okn) break;  // aborting
-      // ---- stage B: publish L(j,j), finish the next step's near-diagonal tiles ----
-      store_tile<NB>(sD, ab, g, j, j);
-      cta_publish(LR(j, 0), 1);
-      if (threadIdx.x == 0) trace_stamp_to(tr, j, 2);
-      if (!next) break;
-      make_dinv(sD);
-      if (has_w) {
-        tile_gemm<NB, true>(sP, sW, sLp);  // A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T
-        tile_gemm<NB, true>(sD2, sW, sW);  // A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
-      } else {
-        __syncthreads();
+      // ---- stage B ----
+      if (warp >= 4) {
+        // write-backs and publishes beside the chain; the two releases (each waits for the
+        // stores before it to be performed, ~1 K cycles) sit in different warps
+        const int t = threadIdx.x - 128;
+        store_tile<NB, 128>(sD, ab, g, j, j, t);
+        store_dense<NB, 128>(sInv, ws.inv + (size_t)j * NB * NB, t);
+        named_sync(3, 128);
+        if (t == 0) st_release(LR(j, 0), 1);  // L(j,j) and its inverse
+        if (next && warp >= 5) {
+          named_sync(4, 224);  // the TRSM product is in sX
+          store_tile<NB, 96>(sX, ab, g, j + 1, j, t - 32);
+          named_sync(8, 96);
+          if (t == 32) st_release(LR(j + 1, 1), 1);
+        }
+      } else if (next) {
+        tile_gemm<NB, false, 4, true>(sX, sP, sInv, warp, 2, 128);  // L(j+1,j) = A(j+1,j) L(j,j)^-T
+        asm volatile("bar.arrive 4, 224;" ::: "memory");
+        if (threadIdx.x == 0) trace_stamp_to(tr, j, 3);
+        tile_gemm<NB, true, 4>(sD2, sX, sX, warp, 2, 128);  // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T
+        if (threadIdx.x == 0) trace_stamp_to(tr, j, 4);
       }
-      if (threadIdx.x == 0) trace_stamp_to(tr, j, 3);
-      if (warp == 0) trsm_rows<NB>(sP, sD, sdinv, threadIdx.x);  // L(j+1,j) = A(j+1,j) L(j,j)^-T
-      __syncthreads();
-      if (threadIdx.x == 0) trace_stamp_to(tr, j, 4);
-      tile_gemm<NB, true>(sD2, sP, sP);  // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T
-      store_tile<NB>(sP, ab, g, j + 1, j);
-      cta_publish(LR(j + 1, 1), 1);
-      if (threadIdx.x == 0) trace_stamp_to(tr, j, 5);
-      // rotate: D <- D2, Lp <- P; free = old D, old Lp, W
+      if (!next) break;
+      // rotate: D <- D2, Lp <- X; free = old D, old Lp, W, P
       double* oldD = sD;
       double* oldLp = sLp;
       sD = sD2;
-      sLp = sP;
+      sLp = sX;
       f0 = oldD;
       f1 = oldLp;
       f2 = sW;
+      f3 = sP;
       __syncthreads();
+      if (threadIdx.x == 0) trace_stamp_to(tr, j, 5);
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
       const int fl = ld_volatile(ws.ctrl + 1);
       info[0] = fail_col >= 0 ? fail_col + 1 : (fl ? fl : 0);
@@ -426,7 +532,6 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   const int grp = warp / GW, gt = threadIdx.x - grp * GT, wg = warp - grp * GW;
   const int bar = 1 + grp;
   __shared__ int s_task2[kGroups], s_ok2[kGroups];
-  __shared__ double sdinv2[kGroups][NB];
   double* sA = smem + grp * 3 * E;
   double* sB = sA + E;
   double* sC = sA + 2 * E;
@@ -490,14 +595,11 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       if (!warp_uniform(s_ok2[grp])) break;
       ph(1);
       load_tile<NB, GT>(sA, ab, g, R, j, gt);
-      load_tile<NB, GT>(sB, ab, g, j, j, gt);
+      load_dense<NB, GT>(sB, ws.inv + (size_t)j * NB * NB, gt);
       gsync();
       ph(2);
-      if (gt < NB) sdinv2[grp][gt] = 1.0 / sB[gt * LD + gt];
-      gsync();
-      if (wg == 0) trsm_rows<NB>(sA, sB, sdinv2[grp], gt);
-      gsync();
-      store_tile<NB, GT>(sA, ab, g, R, j, gt);
+      tile_gemm<NB, false, GW, (GW <= 4)>(sC, sA, sB, wg, bar, GT);  // L(R,j) = A(R,j) L(j,j)^-T as a product
+      store_tile<NB, GT>(sC, ab, g, R, j, gt);
       ph(3);
       gpublish(LR(R, R - j), 1);
       ph(4);
@@ -510,11 +612,11 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         if (!warp_uniform(s_ok2[grp])) break;
         ph(1);
         load_tile<NB, GT>(sB, ab, g, S, j, gt);
-        load_tile<NB, GT>(sC, ab, g, R, S, gt);
+        load_tile<NB, GT>(sA, ab, g, R, S, gt);
         gsync();
         ph(2);
-        tile_gemm<NB, true, GW>(sC, sA, sB, wg, bar, GT);
-        store_tile<NB, GT>(sC, ab, g, R, S, gt);
+        tile_gemm<NB, true, GW>(sA, sC, sB, wg, bar, GT);  // (L(R,j) is still in sC)
+        store_tile<NB, GT>(sA, ab, g, R, S, gt);
         ph(3);
         gpublish(TC(R, R - S), done + 1);
         ph(4);
@@ -581,7 +683,7 @@ inline MultiGeom multi_geom(int n, int kd, int ldab) {
 
 inline size_t multi_workspace_bytes(int n, int kd) {
   MultiGeom g = multi_geom(n, kd, kd + 1);
-  return multi_flag_bytes(g.nblk, g.T);
+  return multi_flag_bytes(g.nblk, g.T) + (size_t)g.nblk * kMultiNB * kMultiNB * sizeof(double);
 }
 
 // Occupancy: wide bands (many worker tasks per step) run 3 CTAs per SM for latency
@@ -591,8 +693,8 @@ inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, vo
                           cudaStream_t st, char* err, size_t errlen) {
   constexpr int NB = kMultiNB;
   MultiGeom g = multi_geom(n, kd, ldab);
-  // pivot: 5 tiles; workers: 3 per group
-  const size_t smem = (size_t)(kGroups == 1 ? 5 : 3 * kGroups) * MultiTile<NB>::ELEMS * sizeof(double);
+  // pivot: 7 tiles; workers: 3 per group
+  const size_t smem = (size_t)(3 * kGroups > 7 ? 3 * kGroups : 7) * MultiTile<NB>::ELEMS * sizeof(double);
   auto k = band_multi_kernel<NB, kPerSM, kGroups>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) {
@@ -625,7 +727,7 @@ inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, vo
 inline int launch_multi(double* ab, int n, int kd, int ldab, int32_t* info, void* workspace, int sms,
                         cudaStream_t st, char* err, size_t errlen) {
   if (kd >= 1000) return launch_multi_t<BCG_WIDE_PERSM, BCG_WIDE_GROUPS>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
-  return launch_multi_t<2, 1>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
+  return launch_multi_t<1, 1>(ab, n, kd, ldab, info, workspace, sms, st, err, errlen);
 }
 
 }  // namespace bcg

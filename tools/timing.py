@@ -141,16 +141,17 @@ def trace(tag):
     t = buf.cpu().numpy()
     steps = int(t[0])
     st = t[1:1 + 8 * steps].reshape(steps, 8).astype(np.float64)
-    d = np.diff(st[:, :6], axis=1)  # phase durations 0->1 .. 4->5
-    nxt = st[1:, 0] - st[:-1, 5]     # gap to next step start
-    names = ["potrf_and_loads", "publish_L", "lookback_gemms", "trsm", "syrk_publish"]
-    out = {"config": tag, "steps": steps, "unit": "cycles", "total_cycles": float(st[-1, 1] - st[0, 0])}
+    # pivot stamps: 0 step start, 1 POTRF done, 2 stage-A barrier passed (lookback done too),
+    # 3 TRSM product done, 4 SYRK done, 5 closing barrier; 6 (service thread) L(j+1,j-1) flag
+    # seen, 7 (warp 2) lookback product done
+    d = np.diff(st[:, :6], axis=1)
+    names = ["potrf", "wait_lookback", "trsm", "syrk", "close"]
+    out = {"config": tag, "steps": steps, "unit": "cycles", "total_cycles": float(st[-1, 1] - st[0, 0]),
+           "step": float(np.median(np.diff(st[:, 0])))}
     for i, nm in enumerate(names):
-        v = d[:-1, i]
-        out[nm] = float(np.median(v))
-    out["gap"] = float(np.median(nxt))
-    out["wait_tc"] = float(np.median(st[:-1, 6] - st[:-1, 0]))
-    out["wait_lr"] = float(np.median(st[:-1, 7] - st[:-1, 6]))
+        out[nm] = float(np.median(d[2:-2, i]))
+    out["flag_w_after_start"] = float(np.median(st[2:-2, 6] - st[2:-2, 0]))
+    out["lookback_done_after_start"] = float(np.median(st[2:-2, 7] - st[2:-2, 0]))
     wk = t[-8:-3].astype(np.float64)
     if wk.sum() > 0:
         out["worker_share"] = {k: round(float(v / wk.sum()), 3)
