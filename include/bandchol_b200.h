@@ -82,11 +82,20 @@ int bcg_dpbtrs_batched_nrhs(int64_t n, int64_t kd, const double* ab, int64_t lda
                             double* b, int64_t ldb, int64_t stride_b, int64_t nrhs, int64_t batch,
                             int32_t* info, void* stream);
 
+/* Workspace bytes of bcg_dpbsv_batched: batch * n doubles (the forward sweep's y, one row
+ * per matrix) when the fused path applies -- 32 <= kd and the band window fits one CTA's
+ * shared memory -- else bcg_dpbtrf_batched_workspace_size.  A smaller (or NULL) workspace is
+ * accepted: the call then runs the unfused path (factorization, two-sweep solve). */
+size_t bcg_dpbsv_batched_workspace_size(int64_t n, int64_t kd, int64_t ldab, int64_t batch);
+
 /* Batched factor + solve (config C5): on return ab holds L and b holds x.  Stream-ordered
- * on `stream`: the batched factorization, then the streamed solve of the matrices that
- * factored.  info: device int32[batch] with the dpbtrf convention; a matrix that fails
- * keeps its b untouched (LAPACK dpbsv) and its ab partially overwritten (as after a
- * failed reference factorization).  workspace as for bcg_dpbtrf_batched. */
+ * on `stream`: the batched factorization -- with the forward sweep L y = b fused in (the
+ * factorization kernel solves each 16-row block right behind its panel, from shared memory,
+ * y to the workspace) -- then the backward sweep of the matrices that factored.
+ * info: device int32[batch] with the dpbtrf convention; a matrix that fails keeps its b
+ * untouched (LAPACK dpbsv) and its ab partially overwritten (as after a failed reference
+ * factorization).  Replaces factor_blocked_serial (pkg/src/bandchol/blocked.py:363-385)
+ * followed by solve_with_factor (pkg/src/bandchol/core.py:216-240) per matrix. */
 int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab,
                       double* b, int64_t stride_b, int64_t batch, int32_t* info,
                       void* workspace, size_t workspace_bytes, void* stream);

@@ -23,6 +23,7 @@ SIGNATURES = {
     "bcg_dpbtrf_workspace_size": (_sz, [_i64, _i64, _i64]),
     "bcg_dpbtrf": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i32p, _vp, _sz, _vp]),
     "bcg_dpbtrf_batched_workspace_size": (_sz, [_i64, _i64, _i64, _i64]),
+    "bcg_dpbsv_batched_workspace_size": (_sz, [_i64, _i64, _i64, _i64]),
     "bcg_dpbtrf_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _i64, _i32p, _vp, _sz, _vp]),
     "bcg_dpbtrs": (ctypes.c_int, [_i64, _i64, _dp, _i64, _dp, _i64, _i64, _i32p, _vp]),
     "bcg_dpbtrs_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _vp]),

@@ -198,11 +198,16 @@ __host__ __device__ inline size_t cta_panel_doubles(int nb_block, const CtaGeom&
   return (size_t)nb_block * g.pld;
 }
 
+// Forward-sweep scratch of the fused factor + forward solve (dpbsv): the accumulator ring
+// (rows j0 .. j0 + kd + 15, a multiple of 16) + two 16-vectors (v = b + acc, y).
+__host__ __device__ inline int cta_fwd_ring(int kd) { return (kd + 16 + 15) / 16 * 16; }
+__host__ __device__ inline size_t cta_fwd_doubles(int kd) { return (size_t)cta_fwd_ring(kd) + 32; }
+
 // Shared-memory footprint (bytes) of one CTA for block size NB.
 __host__ __device__ inline size_t cta_smem_bytes(int nb_block, const CtaGeom& g) {
   // D: two L11 / L11^-1 buffers (the pipelined factorization alternates them by step)
   size_t d = (size_t)g.nslot * g.lds + cta_panel_doubles(nb_block, g) + 2 * (size_t)nb_block * (nb_block + 4) +
-             nb_block;
+             nb_block + cta_fwd_doubles(g.kd);
   return d * sizeof(double) + 64;
 }
 
@@ -239,7 +244,7 @@ struct CtaBand {
   double* D;                 // L11, D[c*kLDD + r] = L(r, c); then L11^-1, D[i*kLDD + j] = Linv(i, j)
   double* lbuf;              // NB doubles: sink for the inverse lanes' column stores
   unsigned long long* bars;  // mbarrier [0]: window loads
-  unsigned long long* sig;   // pipelined factorization: [0] panel ready, [1] column 0 updated, [2 + (k&1)] update done
+  unsigned long long* sig;   // pipelined factorization: [0] panel ready, [1] column 0 updated, [2 + (k&1)] update done, [4] y_k ready
   unsigned phase = 0;        // parity of the next wait on bars[0] (uniform register)
   bool pending = false;      // a load_cols is in flight
   bool fast = false;         // every column chunk meets the bulk-copy alignment rules
@@ -248,6 +253,11 @@ struct CtaBand {
   int pw = 0;                // the POTRF warp
   int wk = -1;               // this warp's worker index 0..5 (-1: pivot or light warp)
   unsigned long long* tr = nullptr;  // trace buffer (block 0 only), see bcg_set_trace
+  // fused forward sweep (dpbsv, pipelined factorization only): the light warp solves
+  // L y = b block by block right behind the panel, from the panel still in shared memory
+  const double* fb = nullptr;  // this matrix's right-hand side (nullptr: factorization only)
+  double* fy = nullptr;        // y out (n doubles)
+  double* fws = nullptr;       // shared scratch: accumulator ring, then v[16], y[16]
 
   // Roles from the hardware warp slot (%warpid & 3 = SMSP): the second CTA on an SM is
   // rotated by one sub-partition (tools/micro/warpid.cu), so warp index alone cannot tell.
@@ -765,7 +775,7 @@ struct CtaBand {
     const int n = g.n, kd = g.kd, lane = threadIdx.x & 31;
     double* const Dbase = D;
     unsigned lph = phase;  // parity of the next window-load completion
-    int s0 = 0;
+    int s0 = 0, ring0 = 0;
     for (int k = 0; k < nblk; ++k) {
       const int j0 = k * NB, nb = min(NB, n - j0);
       const int m = min(kd, n - j0 - nb);
@@ -773,10 +783,6 @@ struct CtaBand {
       if (*s_fail >= 0) break;
       const int tw = 2 * nblk + 2 + k;  // worker 0's trace row (after the backward sweep's)
       if (wk == 0) { trace_stamp(k, 6); trace_stamp(tw, 0); }
-      if (k >= 1 && k * NB + kd < n) {  // the columns update(k) brings in (prefetched at k-1)
-        mbar_wait(bars, lph);
-        lph ^= 1u;
-      }
       if (wk == 0) trace_stamp(tw, 1);
       named_bar(kBarA, 32 * kWorkers);  // update(k-1) done by every worker
       if (wk == 0) trace_stamp(tw, 2);
@@ -793,10 +799,25 @@ struct CtaBand {
       if (lane == 0) mbar_arrive(sig + 1);
       if (wk == 0) trace_stamp(tw, 4);
       named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete (+ the light warp)
+      // the columns update(k) brings into the window (prefetched at step k-1): only the last
+      // tile columns of the rest below touch them -- TRSM(k) and tile column 0 do not -- so
+      // the copy has had those phases to land
+      if (k >= 1 && k * NB + kd < n) {
+        mbar_wait(bars, lph);
+        lph ^= 1u;
+      }
       if (wk == 0) trace_stamp(tw, 5);
       // the rest, starting with the workers that had no column-0 tile
       const int first = (T - 1) % kWorkers;
       update_tiles(s0, j0, nb, m, T, 1 << 20, (wk + kWorkers - first) % kWorkers, kWorkers);
+      if (fb) {
+        // fused forward sweep: acc[rows below] -= X(k) y_k for panel rows 16.. (the light warp
+        // did y_k and rows 0..15 right after barrier B: long done, the wait is a formality)
+        mbar_wait(sig + 4, k & 1);
+        forward_tail(m, ring0, wk);
+        ring0 += NB;
+        if (ring0 >= cta_fwd_ring(kd)) ring0 = 0;
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(sig + 2 + (k & 1));
       if (wk == 0) { trace_stamp(k, 7); trace_stamp(tw, 6); }
@@ -806,22 +827,129 @@ struct CtaBand {
     D = Dbase;
   }
 
+  // Fused forward sweep, light warp, step k, after barrier B (panel k complete: L11^-1(k) in
+  // D[k & 1], the panel X(k) dense in P) -- the block form of core.py:216-240's forward loop:
+  //   forward_head (light warp): y_k = L11^-1 (b_k + acc_k), acc[rows j0+16..j0+31] -= X0(k) y_k.
+  //                 D[k & 1] and P rows 0..15 stay valid until the pivot's POTRF(k+2) / TRSM(k+1),
+  //                 ordered after this warp's sig[1] arrival of step k.
+  //   forward_tail (workers, after their share of update(k)): acc[rows below] -= X(k) y_k for
+  //                 panel rows 16.., which the workers overwrite in TRSM(k+1), after their barrier A.
+  // The light warp's share is kept minimal: measured, anything it runs on the pivots' SM
+  // sub-partition lengthens both CTAs' POTRF chains.
+  __device__ __forceinline__ void forward_head(int j0, int nb, int m, int ring0, const double* Dk, double& bnext) {
+    const int lane = threadIdx.x & 31, i = lane & 15;
+    const int nxf = cta_fwd_ring(g.kd);
+    double* sv = fws + nxf;
+    double* sy = sv + 16;
+    const double bcur = bnext;
+    {
+      const int jn = j0 + NB + i;  // next step's rows, a step ahead of their use
+      bnext = (lane < 16 && jn < g.n) ? fb[jn] : 0.0;
+    }
+    if (lane < 16) {
+      const double a = fws[ring0 + i];
+      fws[ring0 + i] = 0.0;  // the slot's next row starts from zero
+      sv[i] = i < nb ? bcur + a : 0.0;
+    }
+    __syncwarp();
+    double y = 0.0;
+    {
+      const double* dr = Dk + i * kLDD;  // row i of L11^-1 (zeros right of the diagonal)
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 2) {
+        const double2 d2 = *reinterpret_cast<const double2*>(dr + kk);
+        const double2 v2 = *reinterpret_cast<const double2*>(sv + kk);
+        a4[kk & 3] = fma(d2.x, v2.x, a4[kk & 3]);
+        a4[(kk + 1) & 3] = fma(d2.y, v2.y, a4[(kk + 1) & 3]);
+      }
+      y = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    }
+    if (lane < 16) {
+      sy[i] = y;
+      if (i < nb) fy[j0 + i] = y;
+    }
+    __syncwarp();
+    // panel rows 0..15 (lanes 16-31 mirror lanes 0-15 and do not store)
+    if (m > 0) {
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < 16; ++c) a4[c & 3] = fma(P[c * g.pld + i], sy[c], a4[c & 3]);
+      int rs = ring0 + NB + i;
+      if (rs >= nxf) rs -= nxf;
+      if (lane < 16 && i < m) fws[rs] -= (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    }
+    __syncwarp();
+  }
+
+  // worker wid, at the end of its share of update(k): rows 16 + 32 wid + lane of the panel
+  // (row r is always updated by the same thread within a step; steps are ordered by the
+  // workers' barrier A)
+  __device__ __forceinline__ void forward_tail(int m, int ring0, int wid) {
+    const int lane = threadIdx.x & 31;
+    const int r = NB + 32 * wid + lane;
+    if (32 * wid + NB >= m) return;  // (warp-uniform)
+    const int nxf = cta_fwd_ring(g.kd);
+    const double* sy = fws + nxf + 16;
+    const double* pr = P + (r < m ? r : 0);
+    double l[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) l[c] = pr[c * g.pld];
+    double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) {
+      const double2 y2 = *reinterpret_cast<const double2*>(sy + c);
+      a4[c & 3] = fma(l[c], y2.x, a4[c & 3]);
+      a4[(c + 1) & 3] = fma(l[c + 1], y2.y, a4[(c + 1) & 3]);
+    }
+    int rs = ring0 + NB + r;
+    if (rs >= nxf) rs -= nxf;
+    if (r < m) fws[rs] -= (a4[0] + a4[1]) + (a4[2] + a4[3]);
+  }
+
   __device__ int light_loop(int nblk, volatile int* s_fail) {
     const int n = g.n, kd = g.kd;
-    int s0 = 0, nload = 0;
+    int s0 = 0, nload = 0, ring0 = 0;
+    double bnext = 0.0;
+    if (fb) {
+      const int lane = threadIdx.x & 31;
+      bnext = (lane < 16 && lane < n) ? fb[lane] : 0.0;
+    }
     for (int k = 0; k < nblk; ++k) {
       const int j0 = k * NB, nb = min(NB, n - j0);
+      const int m = min(kd, n - j0 - nb);
       mbar_wait(sig, k & 1);
       if (*s_fail >= 0) break;
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(sig + 1);
       named_bar(kBarB, 32 * (kWorkers + 1));  // panel k complete
+      // write-back and prefetch first (the forward step does not read the window), so the
+      // columns update(k+1) needs are in flight while it runs
       light_store(j0, nb, s0);
       const int jlo = j0 + NB + kd;
       if (jlo < n) {
         light_load(jlo, min(n, jlo + NB), slot_from(s0, j0, jlo));
         ++nload;
       }
+      if (fb) {
+#ifdef BCG_TRACE
+        const unsigned long long tf0 = gtime();
+#endif
+        forward_head(j0, nb, m, ring0, D + (k & 1) * NB * kLDD, bnext);
+        if ((threadIdx.x & 31) == 0) mbar_arrive(sig + 4);  // y_k is in shared memory: the workers' forward_tail
+#ifdef BCG_TRACE
+        if (tr && (threadIdx.x & 31) == 0) {  // duration of the forward step (worker-0 trace row, slot 7)
+          const unsigned long long idx = 1 + (unsigned long long)(2 * nblk + 2 + k) * kTracePhases + 7;
+          if (idx < g_trace_cap) tr[idx] = gtime() - tf0;
+        }
+#endif
+        ring0 += NB;
+        if (ring0 >= cta_fwd_ring(kd)) ring0 = 0;
+      }
+      __syncwarp();
+      // After barrier B (the workers arrive before it), so sig[0] never runs two phases ahead
+      // of this warp; after the forward step, so P(k) and D[k & 1] may be overwritten: the
+      // pivot awaits this arrival before TRSM(k+1), and the workers' TRSM(k+1) follows the
+      // pivot's next signal.
+      if ((threadIdx.x & 31) == 0) mbar_arrive(sig + 1);
       s0 += NB;
       if (s0 >= g.nslot) s0 -= g.nslot;
     }
@@ -834,11 +962,14 @@ struct CtaBand {
     const int warp = warp_uniform(threadIdx.x >> 5);
     init_fast();
     for (int idx = threadIdx.x; idx < NB * g.pld; idx += kCtaThreads) P[idx] = 0.0;
+    if (fb)
+      for (int idx = threadIdx.x; idx < (int)cta_fwd_doubles(kd); idx += kCtaThreads) fws[idx] = 0.0;
     if (threadIdx.x == 0) {
       // sig[1] (column 0 done) also counts the light warp's arrival right after it consumed
       // sig[0]: the workers arrive before barrier B, so without it the pivot could complete
       // sig[0] twice before the light warp waited once
       for (int i = 0; i < 4; ++i) mbar_init(sig + i, i == 0 ? 1 : (i == 1 ? kWorkers + 1 : kWorkers));
+      mbar_init(sig + 4, 1);  // y_k ready (fused forward sweep)
       s_fail = -1;
       s_nload = 0;
     }
@@ -863,7 +994,7 @@ struct CtaBand {
     phase ^= (unsigned)s_nload & 1u;
     const int fail = s_fail;
     if (threadIdx.x == 0)
-      for (int i = 0; i < 4; ++i) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(sig + i)) : "memory");
+      for (int i = 0; i < 5; ++i) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(sig + i)) : "memory");
     __syncthreads();
     return fail < 0 ? -1 : fail;
   }

@@ -227,7 +227,8 @@ __device__ __forceinline__ void prep_backward(const double* blk, int rows, int n
 template <int R>
 __global__ void __launch_bounds__(kSweepThreads, R <= 8 ? 2 : 1)
 pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0, int64_t ldb, int64_t stride_b,
-                   int nrhs, int groups, SweepGeom g, int32_t* info, const int32_t* skip, int check_diag) {
+                   int nrhs, int groups, SweepGeom g, int32_t* info, const int32_t* skip, int check_diag,
+                   const double* y0, int64_t stride_y) {
   extern __shared__ __align__(16) double smem[];
   constexpr int kSweepNP = sweep_np(R);
   __shared__ __align__(8) unsigned long long full[8], empty[8], pfull[kSweepNPMax], pempty[kSweepNPMax];
@@ -239,6 +240,9 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   const int r0 = grp * R;
   const int rv = min(R, nrhs - r0);  // valid right-hand sides of this group
   double* bm = b0 + (int64_t)mat * stride_b + (int64_t)r0 * ldb;
+  // y0: the forward sweep already ran (fused into the factorization, y of this matrix at
+  // y0 + mat * stride_y): only the nblk backward steps run, reading y from there
+  const double* ym = y0 ? y0 + (int64_t)mat * stride_y + (int64_t)r0 * ldb : bm;
   if (check_diag) {
     // the reference checks every diagonal entry before any arithmetic (core.py:227-230)
     const int bad = first_nonpositive_diag(ab, g.n, g.ldab);
@@ -277,12 +281,14 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
-  const int nsteps = 2 * nblk;
+  const int nf = y0 ? 0 : nblk;  // forward steps
+  const int nsteps = nf + nblk;
 #ifdef BCG_TRACE
   // phase stamps of CTA 0 (SM cycles), per step s: chain 0 start, 1 waits done, 2 end;
   // far 3 waits done, 4 done; prep 5 substitution done, 6 t's waits done, 7 t published.
   // [0] = steps (written once): no global read per stamp.
-  unsigned long long* const tr = blockIdx.x == 0 ? g_trace : nullptr;
+  // (not in backward-only mode: the fused factorization before it owns the trace buffer)
+  unsigned long long* const tr = (blockIdx.x == 0 && !y0) ? g_trace : nullptr;
   const unsigned long long tcap = g_trace_cap;  // (read once: no global load inside a phase)
   auto stamp = [&](int step, int ph) {
     if (tr && (threadIdx.x & 31) == 0) {
@@ -294,7 +300,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
 #else
   auto stamp = [](int, int) {};
 #endif
-  auto block_of = [&](int s) { return s < nblk ? s : 2 * nblk - 1 - s; };
+  auto block_of = [&](int s) { return s < nf ? s : nf + nblk - 1 - s; };
   auto Lbuf = [&](int s) { return Lring + (size_t)(s % nbuf) * 16 * ldab; };
   auto full_wait = [&](int s) { mbar_wait(&full[s % nbuf], (unsigned)(s / nbuf) & 1u); };
   constexpr int RL = R == 1 ? 1 : R / 2;
@@ -313,7 +319,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
     for (int s = 0; s < nsteps; ++s) {
       const int k = s % nbuf;
       if (s >= nbuf) mbar_wait(&empty[k], (unsigned)(s / nbuf - 1) & 1u);
-      if (s == nblk) mbar_wait(&fwd_done, 0);  // y is complete in global memory
+      if (s == nf && nf > 0) mbar_wait(&fwd_done, 0);  // y is complete in global memory
       const int b = block_of(s), c0 = 16 * b, cols = min(16, n - c0);
       // right-hand-side rows of the block (forward: b, backward: y): 8-byte cp.async (zero fill
       // past n / past the group's right-hand sides).  full[k] completes after 32 lane
@@ -322,7 +328,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
       for (int e = lane; e < 16 * R; e += 32) {
         const int ii = e / R, r = e - ii * R;
         const bool ok = ii < cols && r < rv;
-        cp_async8_zfill(rb + e, ok ? bm + (int64_t)r * ldb + c0 + ii : bm, ok);
+        cp_async8_zfill(rb + e, ok ? ym + (int64_t)r * ldb + c0 + ii : ym, ok);
       }
       double* dst = Lbuf(s);
       const double* src = ab + (int64_t)c0 * ldab;
@@ -358,7 +364,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
     for (int s = warp - 1; s < nsteps; s += kSweepPrepWarps) {
       const int p = s % kSweepNP;
       if (s >= kSweepNP) mbar_wait(&pempty[p], (unsigned)(s / kSweepNP - 1) & 1u);
-      const bool fwd = s < nblk;
+      const bool fwd = s < nf;
       full_wait(s);
       if (fwd && s >= 1) full_wait(s - 1);
       if (fwd && s >= 2) full_wait(s - 2);
@@ -510,7 +516,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
           mbar_arrive(&empty[own]);
           if (s >= 1) mbar_arrive(&empty[(s - 1) % nbuf]);
           if (s >= 2) mbar_arrive(&empty[(s - 2) % nbuf]);
-          if (s == nblk - 1) {
+          if (s == nf - 1) {
             mbar_arrive(&empty[own]);
             mbar_arrive(&empty[own]);
             if (s >= 1) mbar_arrive(&empty[(s - 1) % nbuf]);
@@ -551,7 +557,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
     for (int s = 0; s < nsteps; ++s, kb.next(nbuf)) {
       const int b = block_of(s), c0 = 16 * b;
       const double* blk = Lring + (size_t)kb.slot * 16 * ldab;
-      if (s < nblk) {
+      if (s < nf) {
         mbar_wait(&ydone[s % kSweepNY], (unsigned)(s / kSweepNY) & 1u);
         mbar_wait(&full[kb.slot], kb.par);
         if (fw == 0 && lane == 0) stamp(s, 3);
@@ -730,9 +736,9 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
   // Per block: wait for the prep slot (H_b / G_b^T row i, loaded while t_b is awaited) and
   // for t_b, then out = t_b - M row i . (the previous block's output).
   RingPos pp, qq;              // prep slot and t / output slot of this step
-  int xs = 0;                  // ring slot of row 16*b (backward: the solution ring)
+  int xs = nf ? 0 : (16 * nblk) % nx;  // ring slot of row 16*b (backward: the solution ring)
   for (int s = 0; s < nsteps; ++s) {
-    const bool fwd = s < nblk;
+    const bool fwd = s < nf;
     const int b = block_of(s), c0 = 16 * b, nb = min(16, n - c0);
     if (!fwd) xs = xs == 0 ? nx - 16 : xs - 16;
     stamp(s, 0);
@@ -841,7 +847,7 @@ pbtrs_sweep_kernel(const double* __restrict__ ab0, int64_t stride_ab, double* b0
       }
     }
     stamp(s, 2);
-    if (s == nblk - 1) {
+    if (s == nf - 1) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&fwd_done);  // release: the y stores above -> the producer's loads
     }

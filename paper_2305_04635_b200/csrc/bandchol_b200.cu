@@ -24,11 +24,12 @@ namespace bcg {
 // One CTA per matrix (grid-stride over the batch).
 template <int NB, int KD>
 __global__ void __launch_bounds__(kCtaThreads, 2)
-pbtrf_cta_kernel(double* ab0, int64_t stride_ab, int batch, CtaGeom g, int32_t* info) {
+pbtrf_cta_kernel(double* ab0, int64_t stride_ab, int batch, CtaGeom g, int32_t* info, const double* b0,
+                 int64_t stride_b, double* y0) {
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) unsigned long long bars[1];
   __shared__ int s_sp[kCtaWarps];
-  __shared__ __align__(8) unsigned long long sig[4];
+  __shared__ __align__(8) unsigned long long sig[5];
   if (threadIdx.x == 0) mbar_init(&bars[0], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -44,7 +45,12 @@ pbtrf_cta_kernel(double* ab0, int64_t stride_ab, int batch, CtaGeom g, int32_t* 
     w.win = p; p += (size_t)g.nslot * g.lds;
     w.P = p; p += cta_panel_doubles(NB, g);
     w.D = p; p += 2 * NB * (NB + 4);
-    w.lbuf = p;
+    w.lbuf = p; p += NB;
+    w.fws = p;
+    if (b0) {  // fused forward sweep (dpbsv): y to the caller's workspace, n doubles per matrix
+      w.fb = b0 + (int64_t)mat * stride_b;
+      w.fy = y0 + (int64_t)mat * g.n;
+    }
     w.sig = sig;
     const int fail = w.factor();
     phase = w.phase;
@@ -132,7 +138,8 @@ int cta_block(int n, int kd, int ldab, bcg::CtaGeom* out) {
   return 0;
 }
 
-int launch_cta(double* ab, int64_t sab, int batch, const bcg::CtaGeom& g, int32_t* info, cudaStream_t st) {
+int launch_cta(double* ab, int64_t sab, int batch, const bcg::CtaGeom& g, int32_t* info, cudaStream_t st,
+               const double* b = nullptr, int64_t sb = 0, double* y = nullptr) {
   constexpr int NB = 16;
   const size_t smem = bcg::cta_smem_bytes(NB, g);
   // the C5 band width gets a compile-time-geometry instantiation (constant strides: 3.67 ->
@@ -140,7 +147,7 @@ int launch_cta(double* ab, int64_t sab, int batch, const bcg::CtaGeom& g, int32_
   auto k = bcg::GeomFixed<100>::matches(g) ? bcg::pbtrf_cta_kernel<NB, 100> : bcg::pbtrf_cta_kernel<NB, 0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
-  k<<<batch, bcg::kCtaThreads, smem, st>>>(ab, sab, batch, g, info);
+  k<<<batch, bcg::kCtaThreads, smem, st>>>(ab, sab, batch, g, info, b, sb, y);
   return cuda_status(cudaGetLastError(), "pbtrf_cta_kernel launch");
 }
 
@@ -183,32 +190,37 @@ static int sweep_r(int64_t nrhs) { return nrhs <= 1 ? 1 : nrhs <= 2 ? 2 : nrhs <
 
 template <int R>
 static int launch_sweep_t(const double* ab, int64_t sab, double* b, int64_t ldb, int64_t sb, int nrhs, int batch,
-                          const bcg::SweepGeom& g, int32_t* info, cudaStream_t st, const int32_t* skip) {
+                          const bcg::SweepGeom& g, int32_t* info, cudaStream_t st, const int32_t* skip,
+                          const double* y, int64_t sy) {
   const size_t smem = bcg::sweep_smem_doubles(g, R) * sizeof(double);
   auto k = bcg::pbtrs_sweep_kernel<R>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(pbtrs_sweep)");
   const int groups = (nrhs + R - 1) / R;
   k<<<(unsigned)((int64_t)batch * groups), bcg::kSweepThreads, smem, st>>>(ab, sab, b, ldb, sb, nrhs, groups, g, info,
-                                                                           skip, skip ? 0 : 1);
+                                                                           skip, skip ? 0 : 1, y, sy);
   return cuda_status(cudaGetLastError(), "pbtrs_sweep_kernel launch");
 }
 
 // Solve `batch` systems, each with nrhs right-hand sides (column r of matrix m at
 // b + m*sb + r*ldb).  skip (device, may be NULL): matrices with skip[m] != 0 are left alone
 // (their factorization failed); with skip the diagonal check is not repeated.
+// y (device, may be NULL; nrhs = 1 only): the forward sweep is already done -- y of matrix m at
+// y + m*sy (the fused factorization wrote it) -- and only the backward sweep runs, x to b.
 static int launch_solve(const double* ab, int64_t sab, double* b, int64_t ldb, int64_t sb, int nrhs, int batch,
-                        int n, int kd, int ldab, int32_t* info, cudaStream_t st, const int32_t* skip = nullptr) {
+                        int n, int kd, int ldab, int32_t* info, cudaStream_t st, const int32_t* skip = nullptr,
+                        const double* y = nullptr, int64_t sy = 0) {
   const int R = sweep_r(nrhs);
   const bcg::SweepGeom g = sweep_geom(n, kd, ldab, R);
   if (g.nbuf) {
     switch (R) {
-      case 1: return launch_sweep_t<1>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
-      case 2: return launch_sweep_t<2>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
-      case 8: return launch_sweep_t<8>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
-      default: return launch_sweep_t<16>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip);
+      case 1: return launch_sweep_t<1>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip, y, sy);
+      case 2: return launch_sweep_t<2>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip, y, sy);
+      case 8: return launch_sweep_t<8>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip, y, sy);
+      default: return launch_sweep_t<16>(ab, sab, b, ldb, sb, nrhs, batch, g, info, st, skip, y, sy);
     }
   }
+  if (y) return fail_arg(0, "internal: backward-only solve needs the streamed kernel");
   // wide bands: one CTA per right-hand side straight from L2
   bcg::pbtrs_kernel<<<(unsigned)((int64_t)batch * nrhs), bcg::kCtaThreads, 0, st>>>(ab, sab, b, ldb, sb, nrhs, n, kd,
                                                                                      ldab, info, skip);
@@ -273,6 +285,14 @@ size_t bcg_dpbtrf_batched_workspace_size(int64_t n, int64_t kd, int64_t ldab, in
   return bcg::multi_workspace_bytes((int)n, (int)kd);
 }
 
+size_t bcg_dpbsv_batched_workspace_size(int64_t n, int64_t kd, int64_t ldab, int64_t batch) {
+  if (check_geom(n, kd, ldab) != 0 || batch <= 0) return 0;
+  bcg::CtaGeom g;
+  if (kd >= 32 && cta_block((int)n, (int)kd, (int)ldab, &g) != 0 && sweep_geom((int)n, (int)kd, (int)ldab, 1).nbuf)
+    return (size_t)batch * (size_t)n * sizeof(double);
+  return bcg_dpbtrf_batched_workspace_size(n, kd, ldab, batch);
+}
+
 int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, int64_t batch,
                        int32_t* info, void* workspace, size_t workspace_bytes, void* stream) {
   if (int r = check_geom(n, kd, ldab)) return r;
@@ -304,9 +324,21 @@ int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t s
   if (batch < 0 || batch > INT_MAX) return fail_arg(8, "batch out of range");
   if (!info) return fail_arg(9, "info is NULL");
   if (batch == 0) return 0;
-  // the batched factorization, then the solve, which skips the matrices whose factorization
-  // failed (their b stays untouched, as LAPACK dpbsv leaves B when info > 0).  Fusing the
-  // forward sweep into the factorization's pivot chain measured slower.
+  // Pipelined one-CTA factorization (32 <= kd, window in shared memory) with a workspace for
+  // y: the factorization kernel's light warp runs the forward sweep L y = b right behind each
+  // panel, from shared memory (y to the workspace: b stays untouched until the matrix is
+  // known to have factored), and the solve kernel only sweeps backward.
+  bcg::CtaGeom g;
+  if (kd >= 32 && cta_block((int)n, (int)kd, (int)ldab, &g) != 0 && sweep_geom((int)n, (int)kd, (int)ldab, 1).nbuf &&
+      workspace &&
+      workspace_bytes >= (size_t)batch * (size_t)n * sizeof(double) && !(((uintptr_t)workspace) & 7)) {
+    double* y = (double*)workspace;
+    if (int rc = launch_cta(ab, stride_ab, (int)batch, g, info, (cudaStream_t)stream, b, stride_b, y)) return rc;
+    return launch_solve(ab, stride_ab, b, n, stride_b, 1, (int)batch, (int)n, (int)kd, (int)ldab, info,
+                        (cudaStream_t)stream, info, y, n);
+  }
+  // otherwise: the batched factorization, then the two-sweep solve, which skips the matrices
+  // whose factorization failed (their b stays untouched, as LAPACK dpbsv leaves B when info > 0)
   if (int rc = bcg_dpbtrf_batched(n, kd, ab, ldab, stride_ab, batch, info, workspace, workspace_bytes, stream))
     return rc;
   return launch_solve(ab, stride_ab, b, n, stride_b, 1, (int)batch, (int)n, (int)kd, (int)ldab, info,

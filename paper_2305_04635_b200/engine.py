@@ -221,8 +221,8 @@ def dpbtrs_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, nrhs: i
 
 def dpbsv_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=None, stream=None):
     """Factor + solve of `batch` systems: ab -> L, b -> x (bcg_dpbsv_batched: the batched
-    factorization, then the streamed solve, which skips failed matrices and leaves their b
-    untouched)."""
+    factorization with the forward sweep fused in -- y goes to the workspace -- then the
+    backward sweep, which skips failed matrices and leaves their b untouched)."""
     torch = _torch()
     _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
     _dev(b, torch, torch.float64, n * batch, "b")
@@ -231,7 +231,7 @@ def dpbsv_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=Non
     with _on_device(torch, ab.device):
         st = _stream_for(torch, ab.device, stream)
         lib = _lib.load()
-        need = int(lib.bcg_dpbtrf_batched_workspace_size(n, kd, ldab, batch))
+        need = int(lib.bcg_dpbsv_batched_workspace_size(n, kd, ldab, batch))
         ws = None
         if need:
             with torch.cuda.stream(st):

@@ -279,7 +279,7 @@ def trace_la(tag, batch=1, solve=False):
            "trsm_signal": med(4, 5), "worker_wake": med(5, 6), "worker_step": med(6, 7),
            "step": float(np.median(np.diff(st[:, 0]))),
            "w_load": wmed(0, 1), "w_barA": wmed(1, 2), "w_trsm": wmed(2, 3), "w_col0": wmed(3, 4),
-           "w_barB": wmed(4, 5), "w_rest": wmed(5, 6)}
+           "w_barB": wmed(4, 5), "w_rest": wmed(5, 6), "fwd_step": float(np.median(wt[:, 7]))}
     print(json.dumps(out), flush=True)
 
 
