@@ -55,6 +55,7 @@ struct MultiGeom {
   int nblk;  // ceil(n / NB)
   int T;     // ceil(kd / NB)
   int Q;     // worker tasks per step
+  int owner; // row-owner scheduling of the row tasks (needs spare worker groups: host decides)
 };
 
 // ---- workspace ---------------------------------------------------------------------
@@ -117,6 +118,18 @@ __device__ __forceinline__ void named_sync(int id, int cnt) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
 }
 
+// cross-SM event stamps (trace build): %globaltimer ns into trace row nblk + step
+__device__ __forceinline__ void xstamp(int nblk, int step, int ph) {
+#ifdef BCG_TRACE
+  if (g_trace && step >= 0 && step < nblk) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long idx = 1 + (unsigned long long)(nblk + step) * kTracePhases + ph;
+    if (idx < g_trace_cap - 8) g_trace[idx] = t;
+  }
+#endif
+}
+
 template <int NB>
 struct MultiTile {
   static constexpr int LD = NB + 4;  // LD = 4 (mod 16) doubles: conflict-free DMMA fragments
@@ -126,11 +139,32 @@ struct MultiTile {
 // ---- tile <-> band storage -----------------------------------------------------------
 // smem tile layout: element (r, c) at s[c*LD + r].  Out-of-band / upper / past-n -> 0.
 // Threads t in [0, NT) take part; every thread issues its loads before its stores.
+// Tiles wholly inside the band (1 <= R - C, (R - C) NB + NB - 1 <= kd, all rows < n) take a
+// path without per-element index arithmetic or masks: thread t keeps row t % NB and walks
+// the columns with a constant pointer stride (the instruction stream of the generic path --
+// ~15 instructions per element -- was most of a worker task's time).
+__device__ __forceinline__ bool tile_interior(const MultiGeom& g, int NB, int R, int C) {
+  const int d = R - C;
+  return d >= 1 && d * NB + NB - 1 <= g.kd && R * NB + NB <= g.n;
+}
+
 template <int NB, int NT>
 __device__ __forceinline__ void load_tile(double* s, const double* ab, const MultiGeom& g, int R, int C, int t) {
   constexpr int LD = MultiTile<NB>::LD;
   constexpr int E = (NB * NB + NT - 1) / NT;
   double v[E];
+  if (NT % NB == 0 && tile_interior(g, NB, R, C)) {
+    constexpr int CS = NT / NB;  // columns per sweep of the threads
+    const int r = t % NB, c0 = t / NB;
+    const double* p = ab + (int64_t)(C * NB + c0) * g.ldab + ((R - C) * NB + r - c0);
+    const int64_t step = (int64_t)CS * (g.ldab - 1);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = __ldcg(p + e * step);
+    double* q = s + c0 * LD + r;
+#pragma unroll
+    for (int e = 0; e < E; ++e) q[e * CS * LD] = v[e];
+    return;
+  }
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int idx = t + e * NT;
@@ -147,10 +181,57 @@ __device__ __forceinline__ void load_tile(double* s, const double* ab, const Mul
   }
 }
 
+// tiles (R, C0) -> s0, (R, C1) -> s1 and, with K3, (R, C2) -> s2 in ONE L2 round trip
+template <int NB, int NT, bool K3>
+__device__ __forceinline__ void load_tiles3(double* s0, double* s1, double* s2, const double* ab, const MultiGeom& g,
+                                            int R, int C0, int C1, int C2, int t) {
+  constexpr int LD = MultiTile<NB>::LD;
+  constexpr int E = NB * NB / NT;
+  static_assert(NB * NB % NT == 0 && NT % NB == 0, "whole columns per sweep");
+  constexpr int K = K3 ? 3 : 2;
+  constexpr int CS = NT / NB;
+  const int r = t % NB, c0 = t / NB;
+  double v[K][E];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int C = k == 0 ? C0 : (k == 1 ? C1 : C2);
+    if (tile_interior(g, NB, R, C)) {
+      const double* p = ab + (int64_t)(C * NB + c0) * g.ldab + ((R - C) * NB + r - c0);
+      const int64_t step = (int64_t)CS * (g.ldab - 1);
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[k][e] = __ldcg(p + e * step);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int c = c0 + e * CS;
+        const int i = R * NB + r, j = C * NB + c;
+        const bool ok = (i < g.n) && (i >= j) && (i - j <= g.kd);
+        v[k][e] = ok ? __ldcg(ab + (int64_t)j * g.ldab + (i - j)) : 0.0;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double* q = (k == 0 ? s0 : (k == 1 ? s1 : s2)) + c0 * LD + r;
+#pragma unroll
+    for (int e = 0; e < E; ++e) q[e * CS * LD] = v[k][e];
+  }
+}
+
 template <int NB, int NT = kMultiThreads>
 __device__ __forceinline__ void store_tile(const double* s, double* ab, const MultiGeom& g, int R, int C,
                                            int t = threadIdx.x) {
   constexpr int LD = MultiTile<NB>::LD;
+  if (NT % NB == 0 && tile_interior(g, NB, R, C)) {
+    constexpr int CS = NT / NB, E = NB * NB / NT;
+    const int r = t % NB, c0 = t / NB;
+    double* p = ab + (int64_t)(C * NB + c0) * g.ldab + ((R - C) * NB + r - c0);
+    const int64_t step = (int64_t)CS * (g.ldab - 1);
+    const double* q = s + c0 * LD + r;
+#pragma unroll
+    for (int e = 0; e < E; ++e) __stcg(p + e * step, q[e * CS * LD]);
+    return;
+  }
   for (int idx = t; idx < NB * NB; idx += NT) {
     const int c = idx / NB, r = idx - c * NB;
     const int i = R * NB + r, j = C * NB + c;
@@ -387,32 +468,41 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
     // SYRK of (j+1,j+1); warps 4-7 write back and publish L(j,j), its inverse and L(j+1,j)
     // beside them.  On the chain per step: POTRF, two 32^3 tile products, three barriers.
     __shared__ __align__(8) unsigned long long colbar[8];
-    double* sD = smem;            // current diagonal tile (fully updated)
-    double* sLp = smem + E;       // L(j, j-1) from the previous step
-    double* sInv = smem + 2 * E;  // L(j,j)^-1, sInv[k*LD + c] = Linv(c, k)
-    double* f0 = smem + 3 * E;    // free tiles
-    double* f1 = smem + 4 * E;
-    double* f2 = smem + 5 * E;
-    double* f3 = smem + 6 * E;
+    __shared__ int s_okx;
+    double* sD = smem;             // current diagonal tile (fully updated)
+    double* sLp = smem + E;        // L(j, j-1) from the previous step
+    double* sInv2 = smem + 2 * E;  // L(j,j)^-1 by step parity (sInv[k*LD + c] = Linv(c, k)): the
+                                   // service warps may still be storing the previous one
+    double* sW = smem + 4 * E;     // L(j+1, j-1): the previous step's own TRSM of row j+1
+    double* sP = smem + 5 * E;     // A(j+1, j)
+    double* sD2 = smem + 6 * E;    // A(j+1, j+1)
+    double* sX = smem + 7 * E;     // L(j+1, j)
+    double* sA2 = smem + 8 * E;    // A(j+2, j)
+    double* sX2 = smem + 9 * E;    // L(j+2, j)
+    double* sW2 = smem + 10 * E;   // L(j, j-2): the TRSM of row j two steps ago
+    double* sV = smem + 11 * E;    // L(j+1, j-2) (the row owner's, from global memory)
     unsigned long long* tr = g_trace;
     load_tile<NB, kMultiThreads>(sD, ab, g, 0, 0, threadIdx.x);
     if (threadIdx.x == 0) {
       s_fail = -1;
       s_ok = 1;
+      s_okx = 1;
       for (int i = 0; i < 8; ++i) mbar_init(colbar + i, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     int fail_col = -1;
+    // Per step ONE CTA-wide barrier (between the stages).  Warps 0-3 run the chain -- POTRF,
+    // L^-1, TRSM product, SYRK -- and go straight into the next POTRF; warps 4-7 (service)
+    // follow asynchronously: write-backs and releases of step j overlap POTRF(j+1).
     for (int j = 0; j < nblk; ++j) {
       const int nvalid = min(NB, g.n - j * NB);
-      double* sW = f0;   // L(j+1, j-1)
-      double* sP = f1;   // A(j+1, j)
-      double* sD2 = f2;  // A(j+1, j+1)
-      double* sX = f3;   // L(j+1, j)
+      double* sInv = sInv2 + (j & 1) * E;
       const bool next = j + 1 < nblk;
       const bool has_w = next && (j >= 1) && (T >= 2);
-      if (threadIdx.x == 0) trace_stamp_to(tr, j, 0);
+      const bool has_x2 = (j + 2 < nblk) && (T >= 2);  // row j+2's TRSM is the pivot's too
+      const bool has_v = next && (j >= 2) && (T >= 3);  // A(j+1,j) -= L(j+1,j-2) L(j,j-2)^T is the pivot's
+      if (threadIdx.x == 0) { trace_stamp_to(tr, j, 0); xstamp(nblk, j, 7); }
       // ---- stage A ----
       if (warp == 0) {
         const int f = warp_potrf32(sD, LD, nvalid, sdinv, colbar);
@@ -422,43 +512,47 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         }
       } else if (warp == 1) {
         warp_inverse32(sD, LD, sdinv, sInv, colbar, (unsigned)(j & 1));
-      } else if (next) {
-        if (warp >= 4) {
-          const int t = threadIdx.x - 128;
+      } else if (next && warp != 4 && warp != 5) {
+        // warps 2, 3: the next step's tiles; warps 6, 7 arrive when L(j+1, j-1) (their TRSM of
+        // the previous step) is done; then one lookback product each pair
+        if (warp == 2 || warp == 3) {
+          const int t = threadIdx.x - 64;
           const int lo = max(0, j + 1 - T);
           const int need = max(0, j - 1 - lo);  // worker updates m in [lo, j-2]
+          // A(j+1,j): the workers' updates end at step j-3 -- the one of step j-2 needs
+          // L(j,j-2), this CTA's own TRSM of the step before last, so it is applied here and
+          // not behind a release -> worker -> release round trip
+          const int need1 = has_v ? max(0, j - 2 - lo) : need;
           if (t == 0) {
-            bool ok = spin_ge(TC(j + 1, 1), need, ws.ctrl + 1, 64) && spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
+            bool ok = spin_ge(TC(j + 1, 1), need1, ws.ctrl + 1, 64);
+            ok = ok && spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
+            if (has_v) ok = ok && spin_ge(LR(j + 1, 3), 1, ws.ctrl + 1, 64);
+            trace_stamp_to(tr, j, 6);
             s_ok = ok;
           }
-          named_sync(3, 128);
+          named_sync(6, 64);
           if (warp_uniform(s_ok)) {
-            load_tile<NB, 128>(sP, ab, g, j + 1, j, t);
-            load_tile<NB, 128>(sD2, ab, g, j + 1, j + 1, t);
+            if (has_v) load_tiles3<NB, 64, true>(sP, sD2, sV, ab, g, j + 1, j, j + 1, j - 2, t);
+            else load_tiles3<NB, 64, false>(sP, sD2, nullptr, ab, g, j + 1, j, j + 1, j - 2, t);
           }
-          if (has_w) {
-            if (t == 0 && s_ok) {
-              s_ok = spin_ge(LR(j + 1, 2), 1, ws.ctrl + 1, 64);
-              trace_stamp_to(tr, j, 6);
-            }
-            named_sync(3, 128);
-            if (warp_uniform(s_ok)) load_tile<NB, 128>(sW, ab, g, j + 1, j - 1, t);
-          }
+          if (t == 0) trace_stamp_to(tr, j, 7);  // (tiles loaded)
         }
-        named_sync(5, 192);  // warps 2-7: the tiles are in shared memory
+        if (threadIdx.x == 192) trace_stamp_to(tr, j, 5);  // (warps 6-7 arrive: their TRSM is done)
+        named_sync(5, 128);  // warps 2, 3, 6, 7: the tiles are in shared memory (sW is the pivot's own)
+        if (threadIdx.x == 64) trace_stamp_to(tr, j, 3);   // (lookback products start)
         if (has_w && warp_uniform(s_ok)) {
-          if (warp == 2 || warp == 3) {
-            tile_gemm<NB, true, 2>(sP, sW, sLp, warp - 2, 6, 64);  // A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T
-            if (threadIdx.x == 64) trace_stamp_to(tr, j, 7);
-          } else if (warp >= 6) {
-            tile_gemm<NB, true, 2>(sD2, sW, sW, warp - 6, 7, 64);  // A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
-          }
+          // three products, each on all four warps (two per SM sub-partition 2 / 3: the FP64
+          // pipes of sub-partitions 0 / 1 stay with the POTRF and inverse chains)
+          const int w4 = warp < 4 ? warp - 2 : warp - 4;
+          tile_gemm<NB, true, 4>(sP, sW, sLp, w4, 5, 128);              // A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T
+          tile_gemm<NB, true, 4>(sD2, sW, sW, w4, 5, 128);              // A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
+          if (has_v) tile_gemm<NB, true, 4>(sP, sV, sW2, w4, 5, 128);   // A(j+1,j)   -= L(j+1,j-2) L(j,j-2)^T
         }
       }
       __syncthreads();
       if (threadIdx.x == 0) trace_stamp_to(tr, j, 2);
       const int fl = warp_uniform(s_fail);
-      const int okn = warp_uniform(s_ok);
+      const int okn = warp_uniform(s_ok) && warp_uniform(s_okx);
       if (fl >= 0) {
         fail_col = j * NB + fl;
         if (threadIdx.x == 0) atomicExch(ws.ctrl + 1, fail_col + 1);
@@ -466,39 +560,64 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       }
       if (next && !okn) break;  // aborting
       // ---- stage B ----
-      if (warp >= 4) {
-        // write-backs and publishes beside the chain; the two releases (each waits for the
-        // stores before it to be performed, ~1 K cycles) sit in different warps
+      if (warp == 4) {
+        // the inverse first: every row's TRSM waits for it (L(j,j) itself is only output)
         const int t = threadIdx.x - 128;
-        store_tile<NB, 128>(sD, ab, g, j, j, t);
-        store_dense<NB, 128>(sInv, ws.inv + (size_t)j * NB * NB, t);
-        named_sync(3, 128);
-        if (t == 0) st_release(LR(j, 0), 1);  // L(j,j) and its inverse
-        if (next && warp >= 5) {
-          named_sync(4, 224);  // the TRSM product is in sX
-          store_tile<NB, 96>(sX, ab, g, j + 1, j, t - 32);
-          named_sync(8, 96);
-          if (t == 32) st_release(LR(j + 1, 1), 1);
+        store_dense<NB, 32>(sInv, ws.inv + (size_t)j * NB * NB, t);
+        __syncwarp();
+        if (t == 0) { st_release(LR(j, 0), 1); xstamp(nblk, j + 1, 6); }
+        store_tile<NB, 32>(sD, ab, g, j, j, t);
+        if (has_x2) {
+          named_sync(8, 96);  // warps 6, 7: L(j+2, j) is in sX2 (they go straight on to the lookback)
+          if (warp_uniform(s_okx)) {
+            store_tile<NB, 32>(sX2, ab, g, j + 2, j, t);
+            __syncwarp();
+            if (t == 0) st_release(LR(j + 2, 2), 1);
+          }
+        }
+      } else if (warp == 5) {
+        if (next) {
+          const int t = threadIdx.x - 160;
+          named_sync(4, 160);  // the TRSM product is in sX
+          store_tile<NB, 32>(sX, ab, g, j + 1, j, t);
+          __syncwarp();
+          if (t == 0) st_release(LR(j + 1, 1), 1);
+        }
+      } else if (warp >= 6) {
+        // L(j+2,j) = A(j+2,j) L(j,j)^-T as soon as the row owner's last task has published
+        // A(j+2,j) -- not tied to the stage barrier (the next POTRF and the release of
+        // L(j,j)^-1 do not wait for it): the next step's lookback products read it from shared
+        // memory (these warps join that step's barrier of warps 2-7 when it is done), the
+        // workers' updates of column j+1 from global memory
+        if (has_x2) {
+          const int t = threadIdx.x - 192;
+          if (t == 0) s_okx = spin_ge(TC(j + 2, 2), max(0, j - max(0, j + 2 - T)), ws.ctrl + 1, 64);
+          named_sync(7, 64);
+          if (warp_uniform(s_okx)) {
+            load_tile<NB, 64>(sA2, ab, g, j + 2, j, t);
+            named_sync(7, 64);
+            tile_gemm<NB, false, 2, true>(sX2, sA2, sInv, warp - 6, 7, 64);
+          }
+          asm volatile("bar.arrive 8, 96;" ::: "memory");  // warp 4 writes it back and publishes it
         }
       } else if (next) {
         tile_gemm<NB, false, 4, true>(sX, sP, sInv, warp, 2, 128);  // L(j+1,j) = A(j+1,j) L(j,j)^-T
-        asm volatile("bar.arrive 4, 224;" ::: "memory");
-        if (threadIdx.x == 0) trace_stamp_to(tr, j, 3);
+        asm volatile("bar.arrive 4, 160;" ::: "memory");
         tile_gemm<NB, true, 4>(sD2, sX, sX, warp, 2, 128);  // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T
         if (threadIdx.x == 0) trace_stamp_to(tr, j, 4);
       }
       if (!next) break;
-      // rotate: D <- D2, Lp <- X; free = old D, old Lp, W, P
-      double* oldD = sD;
-      double* oldLp = sLp;
-      sD = sD2;
-      sLp = sX;
-      f0 = oldD;
-      f1 = oldLp;
-      f2 = sW;
-      f3 = sP;
-      __syncthreads();
-      if (threadIdx.x == 0) trace_stamp_to(tr, j, 5);
+      // rotate (every thread for itself, no barrier).  Buffers that lagging warps may still
+      // use: old sD (warp 4's write-back, done before the next stage barrier) becomes sA2,
+      // loaded after that barrier; sX and sX2 (write-backs) become sLp and sW, read-only; old
+      // sA2 (warps 6-7's TRSM input) becomes sX2, their own; old sLp / sW / sP are free since
+      // this step's stage barrier / TRSM and become sP / sD2 / sX.
+      {
+        double* const oD = sD; double* const oLp = sLp; double* const oW = sW; double* const oW2 = sW2;
+        double* const oP = sP; double* const oA2 = sA2;
+        sD = sD2; sLp = sX; sW = sX2; sW2 = oW;
+        sP = oLp; sD2 = oW2; sX = oP; sA2 = oD; sX2 = oA2;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -587,39 +706,81 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
     const int sstep = (int)(t / Q), q = (int)(t - (long long)sstep * Q);
     const int nA = T - 1, nB = T - 1;
     if (q >= nA && q < nA + nB) {
-      const int j = sstep;
-      const int R = j + 2 + (q - nA);
-      if (R >= nblk || j >= nblk) { gsync(); continue; }
-      if (gt == 0) s_ok2[grp] = wait3(LR(j, 0), 1, TC(R, R - j), j - max(0, R - T), nullptr, 0);
-      gsync();
-      if (!warp_uniform(s_ok2[grp])) break;
-      ph(1);
-      load_tile<NB, GT>(sA, ab, g, R, j, gt);
-      load_dense<NB, GT>(sB, ws.inv + (size_t)j * NB * NB, gt);
-      gsync();
-      ph(2);
-      tile_gemm<NB, false, GW, (GW <= 4)>(sC, sA, sB, wg, bar, GT);  // L(R,j) = A(R,j) L(j,j)^-T as a product
-      store_tile<NB, GT>(sC, ab, g, R, j, gt);
-      ph(3);
-      gpublish(LR(R, R - j), 1);
-      ph(4);
-      // the row's update of tile (R, j+1) ((j+2, j+1) is the pivot's)
-      const int S = j + 1;
-      if (R >= j + 3 && S < nblk) {
-        const int done = j - max(0, R - T);
-        if (gt == 0) s_ok2[grp] = wait3(LR(S, 1), 1, TC(R, R - S), done, nullptr, 0);
+      // One row task: TRSM L(R,m) = A(R,m) L(m,m)^-T as a product with the published inverse,
+      // then -- L(R,m) still in sC -- the row's update of tile (R, m+1), the input of its next
+      // TRSM.  resident: A(R,m) is already in sA, complete (left there by the previous task of
+      // the same owner); keep: leave the updated (R, m+1) in sA instead of publishing it.
+      auto row_task = [&](int m, int R, bool resident, bool keep) -> bool {
+        if (gt == 0)
+          s_ok2[grp] = resident ? wait3(LR(m, 0), 1, nullptr, 0, nullptr, 0)
+                                : wait3(LR(m, 0), 1, TC(R, R - m), m - max(0, R - T), nullptr, 0);
         gsync();
-        if (!warp_uniform(s_ok2[grp])) break;
+        if (!warp_uniform(s_ok2[grp])) return false;
         ph(1);
-        load_tile<NB, GT>(sB, ab, g, S, j, gt);
-        load_tile<NB, GT>(sA, ab, g, R, S, gt);
+#ifdef BCG_TRACE
+        const long long rt0 = clock64();
+        if (gt == 0 && m == R - 3) xstamp(nblk, R - 2, 0);
+#endif
+        if (!resident) load_tile<NB, GT>(sA, ab, g, R, m, gt);
+        load_dense<NB, GT>(sB, ws.inv + (size_t)m * NB * NB, gt);
         gsync();
         ph(2);
-        tile_gemm<NB, true, GW>(sA, sC, sB, wg, bar, GT);  // (L(R,j) is still in sC)
-        store_tile<NB, GT>(sA, ab, g, R, S, gt);
+        tile_gemm<NB, false, GW, (GW <= 4)>(sC, sA, sB, wg, bar, GT);
+        store_tile<NB, GT>(sC, ab, g, R, m, gt);
         ph(3);
-        gpublish(TC(R, R - S), done + 1);
+        gpublish(LR(R, R - m), 1);
         ph(4);
+        if (gt == 0 && m == R - 3) xstamp(nblk, R - 2, 1);
+        const int S = m + 1;
+        if (R >= m + 3 && S < nblk) {  // ((m+2, m+1) is the pivot's)
+          const int done = m - max(0, R - T);
+          if (gt == 0) s_ok2[grp] = wait3(LR(S, 1), 1, TC(R, R - S), done, nullptr, 0);
+          gsync();
+          if (!warp_uniform(s_ok2[grp])) return false;
+          ph(1);
+          if (gt == 0 && m == R - 3) xstamp(nblk, R - 2, 2);
+          load_tile<NB, GT>(sB, ab, g, S, m, gt);
+          load_tile<NB, GT>(sA, ab, g, R, S, gt);
+          gsync();
+          ph(2);
+          tile_gemm<NB, true, GW>(sA, sC, sB, wg, bar, GT);
+          if (!keep) {
+            store_tile<NB, GT>(sA, ab, g, R, S, gt);
+            ph(3);
+            gpublish(TC(R, R - S), done + 1);
+            ph(4);
+            if (gt == 0 && m == R - 3) xstamp(nblk, R - 2, 3);
+          }
+        }
+#ifdef BCG_TRACE
+        if (gt == 0 && g_trace && g_trace_cap > 8) {  // row-task latency: sum and count
+          atomicAdd(g_trace + g_trace_cap - 8 + 5, (unsigned long long)(clock64() - rt0));
+          atomicAdd(g_trace + g_trace_cap - 8 + 6, 1ull);
+        }
+#endif
+        return true;
+      };
+      const int R = sstep + 2 + (q - nA);
+      // (row s + 2 is the pivot's: it forms L(s+2, s) itself during its next step)
+      if (R >= nblk || sstep >= nblk || R == sstep + 2) { gsync(); continue; }
+      if (g.owner) {
+        // ROW OWNER: the ticket of the super-step in which row R enters the band (m0) runs the
+        // row's whole chain of tasks m0 .. R-3 on one worker group, the tile between two of them
+        // staying in shared memory: the store -> release -> acquire -> load round trip through
+        // L2 (and the group switch) leaves the row chain TRSM(m) -> update -> TRSM(m+1).  The
+        // last task (m = R-3) publishes tile (R, R-2) for the pivot's own TRSM.  An owner holds
+        // its group for <= T steps; g.owner is set only when the grid has spare groups.
+        const int m0 = max(0, R - T);
+        if (sstep != m0) { gsync(); continue; }
+        bool ok = true, resident = false;
+        for (int m = m0; m <= R - 3 && ok; ++m) {
+          const bool keep = m < R - 3;
+          ok = row_task(m, R, resident, keep);
+          resident = keep;
+        }
+        if (!ok) break;
+      } else {
+        if (!row_task(sstep, R, false, false)) break;
       }
     } else {
       // updates of step s-1: part A (b = a-1: column s+1) or part C (b <= a-2)
@@ -638,7 +799,8 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       }
       const int R = j + 1 + a, S = R - b;
       if (j < 0 || j >= nblk) { gsync(); continue; }
-      const bool pivot_owned = (R == j + 1) || (R == j + 2 && S >= j + 1);
+      // pivot's: rows j+1, j+2 near the diagonal, and (j+3, j+2) (needs the pivot's own L(j+2, j))
+      const bool pivot_owned = (R == j + 1) || (R == j + 2 && S >= j + 1) || (R == j + 3 && S == j + 2 && T >= 3);
       if (R >= nblk || pivot_owned) { gsync(); continue; }
       const int done = j - max(0, R - T);
       if (gt == 0)
@@ -646,6 +808,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       gsync();
       if (!warp_uniform(s_ok2[grp])) break;
       ph(1);
+      if (gt == 0 && R == j + 3 && S == j + 2) xstamp(nblk, j + 2, 4);
       load_tile<NB, GT>(sA, ab, g, R, j, gt);
       load_tile<NB, GT>(sB, ab, g, S, j, gt);
       load_tile<NB, GT>(sC, ab, g, R, S, gt);
@@ -656,6 +819,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       ph(3);
       gpublish(TC(R, R - S), done + 1);
       ph(4);
+      if (gt == 0 && R == j + 3 && S == j + 2) xstamp(nblk, j + 2, 5);
     }
   }
 #ifdef BCG_TRACE
@@ -678,6 +842,7 @@ inline MultiGeom multi_geom(int n, int kd, int ldab) {
   g.nblk = (n + kMultiNB - 1) / kMultiNB;
   g.T = (kd + kMultiNB - 1) / kMultiNB;
   g.Q = (g.T - 1) + g.T * (g.T - 1) / 2;  // per super-step: T-1 row tasks + the step's other updates
+  g.owner = 0;
   return g;
 }
 
@@ -693,8 +858,8 @@ inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, vo
                           cudaStream_t st, char* err, size_t errlen) {
   constexpr int NB = kMultiNB;
   MultiGeom g = multi_geom(n, kd, ldab);
-  // pivot: 7 tiles; workers: 3 per group
-  const size_t smem = (size_t)(3 * kGroups > 7 ? 3 * kGroups : 7) * MultiTile<NB>::ELEMS * sizeof(double);
+  // pivot: 12 tiles; workers: 3 per group
+  const size_t smem = (size_t)(3 * kGroups > 12 ? 3 * kGroups : 12) * MultiTile<NB>::ELEMS * sizeof(double);
   auto k = band_multi_kernel<NB, kPerSM, kGroups>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) {
@@ -715,6 +880,8 @@ inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, vo
   }
   MultiWs ws = multi_ws(workspace, g.nblk, g.T);
   int grid = sms * per_sm;
+  // row owners hold up to T groups at a time: only with at least twice as many (plus slack)
+  g.owner = ((long long)(sms - 1) * per_sm * kGroups >= 2LL * g.T + 16) ? 1 : 0;
   void* args[] = {(void*)&ab, (void*)&g, (void*)&ws, (void*)&info};
   e = cudaLaunchCooperativeKernel((void*)k, dim3(grid), dim3(kMultiThreads), args, smem, st);
   if (e != cudaSuccess) {

@@ -144,14 +144,25 @@ def trace(tag):
     # pivot stamps: 0 step start, 1 POTRF done, 2 stage-A barrier passed (lookback done too),
     # 3 TRSM product done, 4 SYRK done, 5 closing barrier; 6 (service thread) L(j+1,j-1) flag
     # seen, 7 (warp 2) lookback product done
-    d = np.diff(st[:, :6], axis=1)
-    names = ["potrf", "wait_lookback", "trsm", "syrk", "close"]
+    # pivot stamps (SM cycles): 0 step start, 1 POTRF done, 2 stage barrier passed, 4 TRSM + SYRK
+    # done; service: 7 / 6 flags of A(j+1,j) / A(j+1,j+1) seen, 5 warps 6-7 done with the
+    # previous step's TRSM of row j+1, 3 lookback products start
+    rel = lambda k: float(np.median(st[2:-2, k] - st[2:-2, 0]))  # noqa: E731
     out = {"config": tag, "steps": steps, "unit": "cycles", "total_cycles": float(st[-1, 1] - st[0, 0]),
-           "step": float(np.median(np.diff(st[:, 0])))}
-    for i, nm in enumerate(names):
-        out[nm] = float(np.median(d[2:-2, i]))
-    out["flag_w_after_start"] = float(np.median(st[2:-2, 6] - st[2:-2, 0]))
-    out["lookback_done_after_start"] = float(np.median(st[2:-2, 7] - st[2:-2, 0]))
+           "step": float(np.median(np.diff(st[:, 0]))), "potrf_done": rel(1), "stage_barrier": rel(2),
+           "trsm_syrk_done": rel(4), "tiles_loaded": rel(7), "flags_seen": rel(6), "x2_prev_done": rel(5),
+           "lookback_start": rel(3)}
+    if t[-2] > 0:
+        out["row_task_cycles"] = float(t[-3]) / float(t[-2])
+    nb = (n + 31) // 32
+    xs = t[1 + 8 * nb:1 + 16 * nb].reshape(nb, 8).astype(np.float64)[4:-4]
+    ok = (xs[:, 7] > 0) & (xs[:, 0] > 0) & (xs[:, 3] > 0) & (xs[:, 6] > 0)
+    if ok.any():
+        rel = lambda k: float(np.median(xs[ok, k] - xs[ok, 7]))  # noqa: E731  ns after the pivot's step start
+        out["x_ns_after_step_start"] = {"owner_last_linv_seen": rel(0), "owner_last_trsm_published": rel(1),
+                                        "owner_last_deps2_seen": rel(2), "owner_last_tc_published": rel(3),
+                                        "pivot_prev_linv_released": rel(6)}
+        out["step_ns"] = float(np.median(np.diff(xs[:, 7])))
     wk = t[-8:-3].astype(np.float64)
     if wk.sum() > 0:
         out["worker_share"] = {k: round(float(v / wk.sum()), 3)
