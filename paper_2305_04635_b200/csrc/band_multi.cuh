@@ -47,7 +47,7 @@ constexpr int kMultiThreads = 256;
 #endif
 constexpr unsigned kWorkerSpinNs = BCG_WORKER_SPIN_NS;  // longest back-off of a worker's flag spin
 #ifndef BCG_MULTI_PREFETCH
-#define BCG_MULTI_PREFETCH false  // fetch a worker's next ticket while its current task runs
+#define BCG_MULTI_PREFETCH true  // fetch a worker's next ticket while its current update task runs
 #endif
 
 struct MultiGeom {
@@ -656,12 +656,14 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
   double* sC = sA + 2 * E;
   const int Q = g.Q;
   const long long total = (long long)(nblk + 1) * Q;  // super-step nblk: the last rest updates
-  int next_ticket = 0;
-  if (kPrefetchTicket && gt == 0) next_ticket = atomicAdd(ws.ctrl, 1);
+  int held = -1;  // (thread 0 of the group) a ticket fetched early, not yet started
   auto gsync = [&]() { named_sync(bar, GT); };
+  // cumulative release after the group barrier, by the last warp's lane 0: the release waits
+  // until the group's stores are performed (~1 K cycles), and thread 0 spends that time
+  // fetching the next ticket and reading its flags
   auto gpublish = [&](int* flag, int value) {
     gsync();
-    if (gt == 0) st_release(flag, value);  // cumulative release after the group barrier
+    if (gt == GT - 32) st_release(flag, value);
   };
   // one thread: wait for up to three flags (issued together, then spun on one by one)
   auto wait3 = [&](const int* f0, int v0, const int* f1, int v1, const int* f2, int v2) -> bool {
@@ -684,12 +686,8 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
 #endif
   for (;;) {
     if (gt == 0) {
-      if (kPrefetchTicket) {
-        s_task2[grp] = next_ticket;
-        next_ticket = atomicAdd(ws.ctrl, 1);
-      } else {
-        s_task2[grp] = atomicAdd(ws.ctrl, 1);
-      }
+      s_task2[grp] = held >= 0 ? held : atomicAdd(ws.ctrl, 1);
+      held = -1;
     }
     gsync();
     const long long t = warp_uniform(s_task2[grp]);
@@ -808,7 +806,10 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       gsync();
       if (!warp_uniform(s_ok2[grp])) break;
       ph(1);
-      if (gt == 0 && R == j + 3 && S == j + 2) xstamp(nblk, j + 2, 4);
+      // the next ticket while this task's tiles travel (update tasks only: a row owner keeps
+      // its group for many steps and must not sit on an unstarted ticket).  A held ticket
+      // cannot deadlock: this task's dependencies are all on smaller tickets.
+      if (kPrefetchTicket && gt == 0) held = atomicAdd(ws.ctrl, 1);
       load_tile<NB, GT>(sA, ab, g, R, j, gt);
       load_tile<NB, GT>(sB, ab, g, S, j, gt);
       load_tile<NB, GT>(sC, ab, g, R, S, gt);
@@ -819,7 +820,6 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       ph(3);
       gpublish(TC(R, R - S), done + 1);
       ph(4);
-      if (gt == 0 && R == j + 3 && S == j + 2) xstamp(nblk, j + 2, 5);
     }
   }
 #ifdef BCG_TRACE
