@@ -6,12 +6,15 @@ Multi-GPU is STRONG scaling exactly as C5 defines it: the fixed global batch (1,
 --batch B) is partitioned contiguously over the N ranks (sharding.shard), no collective on
 the data path, value = all ranks' matrices / max-over-ranks time.  `--config C1..C4`
 benches a single-matrix config instead (replicas per GPU).  A step = one factor+solve pass
-over the rank's shard through bcg_dpbsv_batched (the factorization kernel, then the
-streamed solve kernel), inputs resident in HBM; a fresh device-to-device copy of the
-pristine inputs is made before every step OUTSIDE the timed events (it also flushes L2:
-3.4 GB > 126 MB).  The two kernels are also timed separately (CUDA events on the launching
-stream) for the per-kernel roofline: the factorization against the FP64 peak (the dominant
-kernel, `roofline`), the solve against HBM (`roofline.kernels.solve`).
+over the rank's shard through bcg_dpbsv_batched (the factorization kernel with the forward
+sweep fused in, then the backward-sweep kernel), inputs resident in HBM; a fresh
+device-to-device copy of the pristine inputs is made before every step OUTSIDE the timed
+events (it also flushes L2: 3.4 GB > 126 MB).  The two kernels are also timed separately
+(CUDA events on the launching stream, through the split entry points
+bcg_dpbtrf_fwd_batched / bcg_dpbtrs_bwd_batched) for the per-kernel roofline: the fused
+factorization against the FP64 peak (the dominant kernel, `roofline`), the backward sweep
+against HBM (`roofline.kernels.solve`); `factor_only` / `solve_two_sweep` are the plain
+factorization and the stand-alone solve for comparison.
 
 Rank 0 prints ONE JSON line (driver contract).  `--impl reference` times the
 reference's own CPU implementation (the unmodified bandchol package installed in
@@ -300,7 +303,7 @@ def run_gpu_arm(args) -> int:
             return 0
         if cfg.batch > 1:
             bc.dpbsv_batched_device(work_a, n, kd, ld, work_b, nb, info=info, stream=stream)
-            return 2  # bcg_dpbsv_batched: the factorization kernel, then the solve kernel
+            return 2  # bcg_dpbsv_batched: factorization + forward sweep kernel, backward sweep kernel
         bc.dpbtrf_device(work_a[0], n, kd, ld, info=info, stream=stream)
         if cfg.solve:
             bc.dpbtrs_device(work_a[0], n, kd, ld, work_b[0], info=info, stream=stream)
@@ -344,26 +347,43 @@ def run_gpu_arm(args) -> int:
     flops_total = n_mat * n * kd * (kd + 3)
     value = flops_total * args.steps / (max_ms * 1e-3) / 1e9  # GFLOP/s, whole job
 
-    # the two kernels of a step timed apart (same stream, CUDA events): factorization, solve
-    fac_ms, sol_ms = [], []
+    # the two kernels of a step timed apart (same stream, CUDA events), exactly as the step
+    # runs them: batched (C5) the factorization with the fused forward sweep
+    # (bcg_dpbtrf_fwd_batched), then the backward sweep (bcg_dpbtrs_bwd_batched); single
+    # matrices the factorization, then the two-sweep solve.  For reference also the plain
+    # batched factorization and the stand-alone two-sweep solve (bcg_dpbtrf_batched,
+    # bcg_dpbtrs_batched).
+    fac_ms, sol_ms, plain_fac_ms, plain_sol_ms = [], [], [], []
+    y_ws = torch.empty_like(b0) if cfg.batch > 1 else None
     for i in range(args.steps if nb else 0):
         refresh()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
         if cfg.batch > 1:
-            bc.dpbtrf_batched_device(work_a, n, kd, ld, nb, info=info, stream=stream)
+            bc.dpbtrf_fwd_batched_device(work_a, n, kd, ld, work_b, y_ws, nb, info=info, stream=stream)
         else:
             bc.dpbtrf_device(work_a[0], n, kd, ld, info=info, stream=stream)
         e1.record(stream)
         if cfg.solve:
             if cfg.batch > 1:
-                bc.dpbtrs_batched_device(work_a, n, kd, ld, work_b, nb, info=info, stream=stream)
+                bc.dpbtrs_bwd_batched_device(work_a, n, kd, ld, y_ws, work_b, nb, info, stream=stream)
             else:
                 bc.dpbtrs_device(work_a[0], n, kd, ld, work_b[0], info=info, stream=stream)
         e2.record(stream)
         torch.cuda.synchronize()
         fac_ms.append(e0.elapsed_time(e1))
         sol_ms.append(e1.elapsed_time(e2))
+        if cfg.batch > 1:
+            refresh()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            bc.dpbtrf_batched_device(work_a, n, kd, ld, nb, info=info, stream=stream)
+            e1.record(stream)
+            bc.dpbtrs_batched_device(work_a, n, kd, ld, work_b, nb, info=info, stream=stream)
+            e2.record(stream)
+            torch.cuda.synchronize()
+            plain_fac_ms.append(e0.elapsed_time(e1))
+            plain_sol_ms.append(e1.elapsed_time(e2))
 
     # end to end through the public API with host buffers (pinned), per rank shard
     solver = bc.BatchedBandSolver(nb, n, kd, chunks=16) if cfg.batch > 1 and nb else None
@@ -419,20 +439,36 @@ def run_gpu_arm(args) -> int:
     else:
         achieved = bytes_rank / (f_ms * 1e-3) / 1e9
         peak, unit = hbm, "GB/s"
+    fused = cfg.batch > 1
+    if fused:
+        # the backward sweep reads L once (the forward sweep ran from shared memory inside the
+        # factorization kernel); the stand-alone solve reads it twice
+        solve_bytes = mats * 8 * n * (kd + 1)
     kernels = {"factor": {"ms": f_ms, "tflops": flops_rank / (f_ms * 1e-3) / 1e12,
-                          "frac_fp64": flops_rank / (f_ms * 1e-3) / 1e9 / fp64_peak}}
+                          "frac_fp64": flops_rank / (f_ms * 1e-3) / 1e9 / fp64_peak,
+                          "what": "factorization + fused forward sweep" if fused else "factorization"}}
     if cfg.solve:
         kernels["solve"] = {"ms": s_ms, "gbs": solve_bytes / (s_ms * 1e-3) / 1e9,
-                            "frac_hbm": solve_bytes / (s_ms * 1e-3) / 1e9 / hbm}
+                            "frac_hbm": solve_bytes / (s_ms * 1e-3) / 1e9 / hbm,
+                            "what": "backward sweep (L read once)" if fused else "two-sweep solve (L read twice)"}
+    if fused and plain_fac_ms:
+        pf, ps = statistics.median(plain_fac_ms), statistics.median(plain_sol_ms)
+        two = mats * 16 * n * (kd + 1)
+        kernels["factor_only"] = {"ms": pf, "tflops": flops_rank / (pf * 1e-3) / 1e12,
+                                  "frac_fp64": flops_rank / (pf * 1e-3) / 1e9 / fp64_peak,
+                                  "what": "bcg_dpbtrf_batched alone"}
+        kernels["solve_two_sweep"] = {"ms": ps, "gbs": two / (ps * 1e-3) / 1e9, "frac_hbm": two / (ps * 1e-3) / 1e9 / hbm,
+                                      "what": "bcg_dpbtrs_batched alone (L read twice)"}
     t_step_roof = max(t_fp, t_hbm) + (solve_bytes / (hbm * 1e9) if cfg.solve else 0.0)
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                "kernel": "factorization (pbtrf_cta_kernel)" if cfg.batch > 1 else "factorization",
+                "kernel": "factorization + fused forward sweep (pbtrf_cta_kernel)" if cfg.batch > 1 else "factorization",
                 "traffic": ncu_traffic(f"{tag}_factor" if cfg.batch > 1 else tag), "kernels": kernels,
                 "step_frac": t_step_roof * 1e3 / step_ms,
                 "step_roof_ms": t_step_roof * 1e3,
                 "peak_source": f"fp64: bcg_probe_fp64_peak DFMA loop (live); hbm: {hbm_src} {hbm:.1f} GB/s",
                 "algorithmic": (f"factor: flops n*kd*(kd+3), bytes 16*n*(kd+1) x {mats} matrices; solve: "
-                                f"bytes 16*n*(kd+1) x {mats} (L read twice)")}
+                                + (f"bytes 8*n*(kd+1) x {mats} (backward sweep, L read once)" if fused
+                                   else f"bytes 16*n*(kd+1) x {mats} (L read twice)"))}
     line = {
         "metric": "fp64 banded Cholesky GFLOP/s (n*kd*(kd+3))", "value": value, "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,

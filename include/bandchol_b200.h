@@ -100,6 +100,22 @@ int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t s
                       double* b, int64_t stride_b, int64_t batch, int32_t* info,
                       void* workspace, size_t workspace_bytes, void* stream);
 
+/* The two halves of bcg_dpbsv_batched's fused path, callable (and timed) on their own.
+ * bcg_dpbtrf_fwd_batched: in-place factorization of the batch with the forward sweep
+ *   L y = b fused in; b is only read, y (device, batch * n doubles, row i = matrix i) is
+ *   written for the matrices -- and up to the block -- that factored.  Needs 32 <= kd and a
+ *   band window that fits one CTA's shared memory (else a negative argument code).
+ * bcg_dpbtrs_bwd_batched: L^T x = y for the matrices with info[i] == 0 (the others are left
+ *   alone), x to x + i*stride_x.  Together they replace factor_blocked_serial
+ *   (pkg/src/bandchol/blocked.py:363-385) + solve_with_factor (pkg/src/bandchol/core.py:216-240),
+ *   whose forward loop (:231-235) and backward loop (:236-239) they split. */
+int bcg_dpbtrf_fwd_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab,
+                           const double* b, int64_t stride_b, int64_t batch, int32_t* info,
+                           double* y, void* stream);
+int bcg_dpbtrs_bwd_batched(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab,
+                           const double* y, double* x, int64_t stride_x, int64_t batch,
+                           int32_t* info, void* stream);
+
 /* Diagnostics: per-step phase timestamps of the whole-GPU factorization, the
  * analogue of the reference's per-task trace (pkg/src/bandchol/parallel.py:54-62).
  * Subsequent bcg_dpbtrf launches on the multi-CTA path write uint64 %globaltimer

@@ -9,7 +9,8 @@ added for the interior-point use case.
 """
 
 from .core import BandedMatrix, index_map
-from .engine import (BatchedBandSolver, TraceEvent, pinned_empty, dpbsv_batched_device, dpbtrf_batched_device, dpbtrf_device,
+from .engine import (BatchedBandSolver, TraceEvent, pinned_empty, dpbsv_batched_device, dpbtrf_fwd_batched_device,
+                     dpbtrs_bwd_batched_device, dpbtrf_batched_device, dpbtrf_device,
                      dpbtrs_batched_device, dpbtrs_device, factor_batched,
                      factor_blocked_parallel, factor_blocked_serial, factor_solve_batched,
                      library_version, solve_batched, solve_many, solve_with_factor)
@@ -24,7 +25,7 @@ from .inputs import CONFIGS, BandConfig, generate_spd, generate_spd_wide, make_r
 __version__ = "0.1.0"
 
 __all__ = [
-    "BandedMatrix", "index_map", "TraceEvent", "BatchedBandSolver", "pinned_empty", "dpbsv_batched_device", "dpbtrf_batched_device",
+    "BandedMatrix", "index_map", "TraceEvent", "BatchedBandSolver", "pinned_empty", "dpbsv_batched_device", "dpbtrf_fwd_batched_device", "dpbtrs_bwd_batched_device", "dpbtrf_batched_device",
     "dpbtrf_device", "dpbtrs_batched_device", "dpbtrs_device", "factor_batched",
     "factor_blocked_parallel", "factor_blocked_serial", "factor_solve_batched", "library_version",
     "solve_batched", "solve_many", "solve_with_factor", "BandCholError", "BandwidthNotDivisible", "CountOverflow",

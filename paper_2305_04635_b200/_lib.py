@@ -30,6 +30,8 @@ SIGNATURES = {
     "bcg_dpbtrs_batched_nrhs": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i64, _i64, _i32p,
                                                _vp]),
     "bcg_dpbsv_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _vp, _sz, _vp]),
+    "bcg_dpbtrf_fwd_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _i64, _i64, _i32p, _dp, _vp]),
+    "bcg_dpbtrs_bwd_batched": (ctypes.c_int, [_i64, _i64, _dp, _i64, _i64, _dp, _dp, _i64, _i64, _i32p, _vp]),
     "bcg_probe_fp64_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
     "bcg_set_trace": (ctypes.c_int, [_vp, _sz]),
     "bcg_band_residual_workspace_size": (_sz, []),

@@ -285,11 +285,16 @@ size_t bcg_dpbtrf_batched_workspace_size(int64_t n, int64_t kd, int64_t ldab, in
   return bcg::multi_workspace_bytes((int)n, (int)kd);
 }
 
+// fused path of bcg_dpbsv_batched: pipelined one-CTA factorization (32 <= kd, window in shared
+// memory) and the streamed solve kernel both apply
+static bool dpbsv_fused(int n, int kd, int ldab, bcg::CtaGeom* g) {
+  return kd >= 32 && cta_block(n, kd, ldab, g) != 0 && sweep_geom(n, kd, ldab, 1).nbuf != 0;
+}
+
 size_t bcg_dpbsv_batched_workspace_size(int64_t n, int64_t kd, int64_t ldab, int64_t batch) {
   if (check_geom(n, kd, ldab) != 0 || batch <= 0) return 0;
   bcg::CtaGeom g;
-  if (kd >= 32 && cta_block((int)n, (int)kd, (int)ldab, &g) != 0 && sweep_geom((int)n, (int)kd, (int)ldab, 1).nbuf)
-    return (size_t)batch * (size_t)n * sizeof(double);
+  if (dpbsv_fused((int)n, (int)kd, (int)ldab, &g)) return (size_t)batch * (size_t)n * sizeof(double);
   return bcg_dpbtrf_batched_workspace_size(n, kd, ldab, batch);
 }
 
@@ -313,9 +318,8 @@ int bcg_dpbtrf_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t 
 }
 
 
-int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, double* b,
-                      int64_t stride_b, int64_t batch, int32_t* info, void* workspace, size_t workspace_bytes,
-                      void* stream) {
+static int check_dpbsv_args(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab, const double* b,
+                            int64_t stride_b, int64_t batch, const int32_t* info) {
   if (int r = check_geom(n, kd, ldab)) return r;
   if (!ab) return fail_arg(3, "ab is NULL");
   if (stride_ab < ldab * n) return fail_arg(5, "stride_ab < ldab*n");
@@ -323,19 +327,46 @@ int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t s
   if (stride_b < n) return fail_arg(7, "stride_b < n");
   if (batch < 0 || batch > INT_MAX) return fail_arg(8, "batch out of range");
   if (!info) return fail_arg(9, "info is NULL");
-  if (batch == 0) return 0;
-  // Pipelined one-CTA factorization (32 <= kd, window in shared memory) with a workspace for
-  // y: the factorization kernel's light warp runs the forward sweep L y = b right behind each
-  // panel, from shared memory (y to the workspace: b stays untouched until the matrix is
-  // known to have factored), and the solve kernel only sweeps backward.
+  return 0;
+}
+
+int bcg_dpbtrf_fwd_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, const double* b,
+                           int64_t stride_b, int64_t batch, int32_t* info, double* y, void* stream) {
+  if (int r = check_dpbsv_args(n, kd, ab, ldab, stride_ab, b, stride_b, batch, info)) return r;
+  if (!y || (((uintptr_t)y) & 7)) return fail_arg(10, "y is NULL or misaligned");
   bcg::CtaGeom g;
-  if (kd >= 32 && cta_block((int)n, (int)kd, (int)ldab, &g) != 0 && sweep_geom((int)n, (int)kd, (int)ldab, 1).nbuf &&
-      workspace &&
+  if (!dpbsv_fused((int)n, (int)kd, (int)ldab, &g))
+    return fail_arg(2, "fused factorization + forward sweep needs 32 <= kd and a band window that fits one CTA");
+  if (batch == 0) return 0;
+  return launch_cta(ab, stride_ab, (int)batch, g, info, (cudaStream_t)stream, b, stride_b, y);
+}
+
+int bcg_dpbtrs_bwd_batched(int64_t n, int64_t kd, const double* ab, int64_t ldab, int64_t stride_ab, const double* y,
+                           double* x, int64_t stride_x, int64_t batch, int32_t* info, void* stream) {
+  if (int r = check_dpbsv_args(n, kd, ab, ldab, stride_ab, x, stride_x, batch, info)) return r;
+  if (!y) return fail_arg(6, "y is NULL");
+  if (sweep_geom((int)n, (int)kd, (int)ldab, 1).nbuf == 0)
+    return fail_arg(2, "the backward-only sweep needs a band whose 16-column ring fits shared memory");
+  if (batch == 0) return 0;
+  return launch_solve(ab, stride_ab, x, n, stride_x, 1, (int)batch, (int)n, (int)kd, (int)ldab, info,
+                      (cudaStream_t)stream, info, y, n);
+}
+
+int bcg_dpbsv_batched(int64_t n, int64_t kd, double* ab, int64_t ldab, int64_t stride_ab, double* b,
+                      int64_t stride_b, int64_t batch, int32_t* info, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+  if (int r = check_dpbsv_args(n, kd, ab, ldab, stride_ab, b, stride_b, batch, info)) return r;
+  if (batch == 0) return 0;
+  // With a workspace for y: the factorization kernel's light warp runs the forward sweep
+  // L y = b right behind each panel, from shared memory (y to the workspace: b stays untouched
+  // until the matrix is known to have factored), and the solve kernel only sweeps backward,
+  // skipping the matrices that failed.
+  bcg::CtaGeom g;
+  if (dpbsv_fused((int)n, (int)kd, (int)ldab, &g) && workspace &&
       workspace_bytes >= (size_t)batch * (size_t)n * sizeof(double) && !(((uintptr_t)workspace) & 7)) {
     double* y = (double*)workspace;
-    if (int rc = launch_cta(ab, stride_ab, (int)batch, g, info, (cudaStream_t)stream, b, stride_b, y)) return rc;
-    return launch_solve(ab, stride_ab, b, n, stride_b, 1, (int)batch, (int)n, (int)kd, (int)ldab, info,
-                        (cudaStream_t)stream, info, y, n);
+    if (int rc = bcg_dpbtrf_fwd_batched(n, kd, ab, ldab, stride_ab, b, stride_b, batch, info, y, stream)) return rc;
+    return bcg_dpbtrs_bwd_batched(n, kd, ab, ldab, stride_ab, y, b, stride_b, batch, info, stream);
   }
   // otherwise: the batched factorization, then the two-sweep solve, which skips the matrices
   // whose factorization failed (their b stays untouched, as LAPACK dpbsv leaves B when info > 0)

@@ -245,6 +245,39 @@ def dpbsv_batched_device(ab, n: int, kd: int, ldab: int, b, batch: int, info=Non
     return info
 
 
+def dpbtrf_fwd_batched_device(ab, n: int, kd: int, ldab: int, b, y, batch: int, info=None, stream=None):
+    """First half of dpbsv_batched_device's fused path (bcg_dpbtrf_fwd_batched): ab -> L with
+    the forward sweep L y = b fused into the factorization kernel; b is only read, y
+    (batch * n doubles) receives the intermediate vectors."""
+    torch = _torch()
+    _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
+    _dev(b, torch, torch.float64, n * batch, "b")
+    _dev(y, torch, torch.float64, n * batch, "y")
+    info = _info(torch, info, batch, ab.device)
+    _same_device(ab.device, b=b, y=y, info=info)
+    with _on_device(torch, ab.device):
+        st = _stream_for(torch, ab.device, stream)
+        rc = _lib.load().bcg_dpbtrf_fwd_batched(n, kd, ab.data_ptr(), ldab, ldab * n, b.data_ptr(), n, batch,
+                                                info.data_ptr(), y.data_ptr(), st.cuda_stream)
+    _lib.check(rc, "bcg_dpbtrf_fwd_batched")
+    return info
+
+
+def dpbtrs_bwd_batched_device(ab, n: int, kd: int, ldab: int, y, x, batch: int, info, stream=None):
+    """Second half (bcg_dpbtrs_bwd_batched): L^T x = y for the matrices with info == 0."""
+    torch = _torch()
+    _dev(ab, torch, torch.float64, ldab * n * batch, "ab")
+    _dev(y, torch, torch.float64, n * batch, "y")
+    _dev(x, torch, torch.float64, n * batch, "x")
+    _same_device(ab.device, y=y, x=x, info=info)
+    with _on_device(torch, ab.device):
+        st = _stream_for(torch, ab.device, stream)
+        rc = _lib.load().bcg_dpbtrs_bwd_batched(n, kd, ab.data_ptr(), ldab, ldab * n, y.data_ptr(), x.data_ptr(), n,
+                                                batch, info.data_ptr(), st.cuda_stream)
+    _lib.check(rc, "bcg_dpbtrs_bwd_batched")
+    return info
+
+
 def band_residual_device(a, l, n: int, kd: int, lda: int, ldl: int, out=None, stream=None):
     """Device ||A - L L^T||_F / ||A||_F (core.py:186-213) of CUDA float64 tensors; returns
     a 1-element CUDA tensor (no host synchronisation)."""
