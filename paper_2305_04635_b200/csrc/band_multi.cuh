@@ -31,6 +31,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "band_cta.cuh"
@@ -882,6 +883,9 @@ inline int launch_multi_t(double* ab, int n, int kd, int ldab, int32_t* info, vo
   int grid = sms * per_sm;
   // row owners hold up to T groups at a time: only with at least twice as many (plus slack)
   g.owner = ((long long)(sms - 1) * per_sm * kGroups >= 2LL * g.T + 16) ? 1 : 0;
+  if (const char* e = getenv("BCG_MULTI_NO_OWNER")) {  // (tests: the one-ticket-per-link fallback)
+    if (e[0] == '1') g.owner = 0;
+  }
   void* args[] = {(void*)&ab, (void*)&g, (void*)&ws, (void*)&info};
   e = cudaLaunchCooperativeKernel((void*)k, dim3(grid), dim3(kMultiThreads), args, smem, st);
   if (e != cudaSuccess) {

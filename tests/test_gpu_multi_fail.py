@@ -83,3 +83,22 @@ def test_batched_whole_gpu_path_reports_member():
     with pytest.raises(bc.NotPositiveDefinite) as err:
         bc.factor_batched(data, n, k)
     assert err.value.matrix == 1 and err.value.column == 1234
+
+
+@pytest.mark.parametrize("n,k", GEOMS)
+def test_row_owner_and_per_link_scheduling_agree(n, k, monkeypatch):
+    """Row-owner scheduling (one worker group runs a row's whole TRSM/update chain) and the
+    one-ticket-per-link fallback (grids without spare groups; forced with BCG_MULTI_NO_OWNER)
+    apply the same updates in the same order: identical bytes, and failures come back alike."""
+    base = generate_spd(n, k, 4).data
+    ws = torch.zeros(int(_lib.load().bcg_dpbtrf_workspace_size(n, k, k + 1)), dtype=torch.uint8, device="cuda")
+    info_o, with_owner = _factor_on(ws, base, n, k)
+    monkeypatch.setenv("BCG_MULTI_NO_OWNER", "1")
+    info_l, per_link = _factor_on(ws, base, n, k)
+    assert info_o == 0 and info_l == 0
+    assert with_owner.tobytes() == per_link.tobytes()
+    bad = base.copy()
+    col = n // 2 + 5
+    bad[col * (k + 1)] = float("nan")
+    info, _ = _factor_on(ws, bad, n, k)
+    assert info == col + 1

@@ -245,7 +245,8 @@ void probe(int noise) {
 
 int main() {
   for (int m : {0x00, 0xe2, 0xe3, 0xe1, 0x12, 0xf3}) probe(m);
-  const int masks[] = {0x00, 0x11, 0x14, 0x18, 0xe4, 0xe8, 0xe3};
+  const int masks[] = {0x00, 0xe1, 0x11, 0x14, 0xe2, 0xe3, 0xf3};
   for (int m : masks) run<0>("v0 production", m);
+  for (int m : masks) run<1>("v2 three-row lookahead", m);
   return 0;
 }
