@@ -264,13 +264,17 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
   const int wm = warp % WM, wn = warp / WM;
   const int gr = lane >> 2, gc = lane & 3;
   double acc[TM][TN][2];
+  // B columns / C column pairs in the kperm order (band_cta.cuh): with LD = 4 (mod 16) doubles
+  // the C fragment loads and stores of a half-warp then hit 16 distinct bank pairs (the
+  // identity order is 2-way conflicted: 25 % of the kernel's shared-memory wavefronts on C4)
+  const int pb = kperm(gr), pc0 = kperm(2 * gc), pc1 = kperm(2 * gc + 1);
 #pragma unroll
   for (int tm = 0; tm < TM; ++tm)
 #pragma unroll
     for (int tn = 0; tn < TN; ++tn) {
-      const int m = (wm * TM + tm) * 8 + gr, nn = (wn * TN + tn) * 8 + 2 * gc;
-      acc[tm][tn][0] = kSub ? sC[nn * LD + m] : 0.0;
-      acc[tm][tn][1] = kSub ? sC[(nn + 1) * LD + m] : 0.0;
+      const int m = (wm * TM + tm) * 8 + gr, n0 = (wn * TN + tn) * 8;
+      acc[tm][tn][0] = kSub ? sC[(n0 + pc0) * LD + m] : 0.0;
+      acc[tm][tn][1] = kSub ? sC[(n0 + pc1) * LD + m] : 0.0;
     }
 #pragma unroll
   for (int k0 = 0; k0 < NB; k0 += 4) {
@@ -281,7 +285,7 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
       a[tm] = kSub ? -v : v;
     }
 #pragma unroll
-    for (int tn = 0; tn < TN; ++tn) b[tn] = sB[(k0 + gc) * LD + (wn * TN + tn) * 8 + gr];
+    for (int tn = 0; tn < TN; ++tn) b[tn] = sB[(k0 + gc) * LD + (wn * TN + tn) * 8 + pb];
 #pragma unroll
     for (int tm = 0; tm < TM; ++tm)
 #pragma unroll
@@ -295,9 +299,9 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
   for (int tm = 0; tm < TM; ++tm)
 #pragma unroll
     for (int tn = 0; tn < TN; ++tn) {
-      const int m = (wm * TM + tm) * 8 + gr, nn = (wn * TN + tn) * 8 + 2 * gc;
-      sC[nn * LD + m] = acc[tm][tn][0];
-      sC[(nn + 1) * LD + m] = acc[tm][tn][1];
+      const int m = (wm * TM + tm) * 8 + gr, n0 = (wn * TN + tn) * 8;
+      sC[(n0 + pc0) * LD + m] = acc[tm][tn][0];
+      sC[(n0 + pc1) * LD + m] = acc[tm][tn][1];
     }
   named_sync(bar_id, bar_cnt);
 }
