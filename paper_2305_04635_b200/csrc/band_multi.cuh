@@ -148,6 +148,12 @@ __device__ __forceinline__ bool tile_interior(const MultiGeom& g, int NB, int R,
   const int d = R - C;
   return d >= 1 && d * NB + NB - 1 <= g.kd && R * NB + NB <= g.n;
 }
+// A diagonal tile may be LOADED without masks as well: its entries above the diagonal then
+// come from the preceding columns' storage (in bounds for R >= 1), and every consumer treats
+// the upper triangle as don't-care (POTRF, the SYRK-type products; write-backs are masked).
+__device__ __forceinline__ bool tile_loadable_unmasked(const MultiGeom& g, int NB, int R, int C) {
+  return tile_interior(g, NB, R, C) || (R == C && R >= 1 && NB - 1 <= g.kd && R * NB + NB <= g.n);
+}
 
 template <int NB, int NT>
 __device__ __forceinline__ void load_tile(double* s, const double* ab, const MultiGeom& g, int R, int C, int t) {
@@ -196,7 +202,7 @@ __device__ __forceinline__ void load_tiles3(double* s0, double* s1, double* s2, 
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int C = k == 0 ? C0 : (k == 1 ? C1 : C2);
-    if (tile_interior(g, NB, R, C)) {
+    if (tile_loadable_unmasked(g, NB, R, C)) {
       const double* p = ab + (int64_t)(C * NB + c0) * g.ldab + ((R - C) * NB + r - c0);
       const int64_t step = (int64_t)CS * (g.ldab - 1);
 #pragma unroll
