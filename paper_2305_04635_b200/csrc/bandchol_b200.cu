@@ -142,9 +142,14 @@ int launch_cta(double* ab, int64_t sab, int batch, const bcg::CtaGeom& g, int32_
                const double* b = nullptr, int64_t sb = 0, double* y = nullptr) {
   constexpr int NB = 16;
   const size_t smem = bcg::cta_smem_bytes(NB, g);
-  // the C5 band width gets a compile-time-geometry instantiation (constant strides: 3.67 ->
-  // 3.51 ms for 1024 matrices); other widths keep the runtime geometry
-  auto k = bcg::GeomFixed<100>::matches(g) ? bcg::pbtrf_cta_kernel<NB, 100> : bcg::pbtrf_cta_kernel<NB, 0>;
+  // common band widths get a compile-time-geometry instantiation (constant strides: C5
+  // 3.67 -> 3.51 ms for 1024 matrices); other widths keep the runtime geometry
+  // (a small set of band widths, each ~4-5 % faster than the runtime geometry; ldab = kd + 1)
+  auto k = bcg::pbtrf_cta_kernel<NB, 0>;
+  if (bcg::GeomFixed<100>::matches(g)) k = bcg::pbtrf_cta_kernel<NB, 100>;
+  else if (bcg::GeomFixed<50>::matches(g)) k = bcg::pbtrf_cta_kernel<NB, 50>;
+  else if (bcg::GeomFixed<64>::matches(g)) k = bcg::pbtrf_cta_kernel<NB, 64>;
+  else if (bcg::GeomFixed<128>::matches(g)) k = bcg::pbtrf_cta_kernel<NB, 128>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
   k<<<batch, bcg::kCtaThreads, smem, st>>>(ab, sab, batch, g, info, b, sb, y);

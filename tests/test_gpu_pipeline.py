@@ -95,10 +95,11 @@ def test_pipelined_odd_shapes_factor_and_solve(n, k, ld):
     assert np.linalg.norm(dvb.cpu().numpy()[0] - xs) <= X_TOL * np.linalg.norm(xs)
 
 
-def test_compile_time_geometry_matches_runtime_geometry():
-    """kd = 100 with ldab = 101 runs the GeomFixed<100> instantiation, a padded ldab the runtime
-    one: the same arithmetic in the same order, so L must agree bit for bit."""
-    n, k, B = 1200, 100, 5
+@pytest.mark.parametrize("k", [100, 50, 64, 128])
+def test_compile_time_geometry_matches_runtime_geometry(k):
+    """kd in {50, 64, 100, 128} with ldab = kd + 1 runs a GeomFixed<kd> instantiation, a padded
+    ldab the runtime one: the same arithmetic in the same order, so L must agree bit for bit."""
+    n, B = 1200, 5
     data = np.stack([generate_spd(n, k, s).data for s in range(B)])
     a = torch.from_numpy(data.copy()).cuda()
     assert int(bc.dpbtrf_batched_device(a, n, k, k + 1, B).abs().sum().item()) == 0
