@@ -196,6 +196,54 @@ __global__ void latprobe(long long* out, int noise, int iters) {
   out[8 + lane] = (long long)x + idx;
 }
 
+// the production function itself (CtaBand<16,100>::potrf_diag) on a real ring window: prologue
+// (rows from the ring), column loop, epilogue (L back to the ring, L^-1 to D)
+__global__ void lab_prod(const double* gA, long long* cyc, int iters, int s0, int noise) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int stop, piv;
+  CtaGeom g;
+  g.n = 1 << 20; g.kd = 100; g.ldab = 101; g.lds = 101; g.nslot = 116; g.pld = 100;
+  CtaBand<16, 100> w{g};
+  w.win = sm;
+  w.P = sm + 116 * 101;
+  w.D = w.P + 1600;
+  w.lbuf = w.D + 640;
+  double* nbuf = w.lbuf + 64;
+  if (threadIdx.x == 0) { stop = 0; unsigned h; asm volatile("mov.u32 %0, %%warpid;" : "=r"(h)); piv = h & 3; }
+  if (noise) for (int t = threadIdx.x; t < 8 * 1024; t += blockDim.x) nbuf[t] = 1e-6 * (t % 13);
+  __syncthreads();
+  if (threadIdx.x >= 32) {
+    const int wq = threadIdx.x >> 5;
+    unsigned hw;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(hw));
+    if ((noise >> (4 + ((hw - piv) & 3))) & 1) noise_loop(noise & 15, &stop, nbuf + wq * 1024, (double*)(cyc + 64));
+    return;
+  }
+  const int r = threadIdx.x;
+  auto fill = [&]() {
+    if (r < 16)
+      for (int c = 0; c <= r; ++c) {
+        const int sl = (s0 + c) % 116;
+        w.win[sl * 101 + (r - c)] = gA[c * 16 + r];
+      }
+    __syncwarp();
+  };
+  fill();
+  int f = w.potrf_diag(s0, 4096, 16);
+  long long tf = 0, tp = 0;
+  for (int it = 0; it < iters; ++it) {
+    long long t0 = clock64();
+    fill();
+    long long t1 = clock64();
+    f += w.potrf_diag(s0, 4096, 16);
+    long long t2 = clock64();
+    tf += t1 - t0;
+    tp += t2 - t1;
+  }
+  if (r == 0) { cyc[0] = tp / iters; cyc[1] = tf / iters; cyc[2] = f; }
+  stop = 1;
+}
+
 template <int V>
 void run(const char* name, int noise = 0) {
   constexpr int N = variant_n<V>();
@@ -245,6 +293,29 @@ void probe(int noise) {
 
 int main() {
   for (int m : {0x00, 0xe2, 0xe3, 0xe1, 0x12, 0xf3}) probe(m);
+  {
+    const int N = 16;
+    std::vector<double> a(N * N);
+    srand(1);
+    for (int c = 0; c < N; ++c)
+      for (int r2 = c + 1; r2 < N; ++r2) { double v = 2.0 * rand() / RAND_MAX - 1.0; a[c * N + r2] = v; a[r2 * N + c] = v; }
+    for (int r2 = 0; r2 < N; ++r2) { double sum = 1.0; for (int c = 0; c < N; ++c) if (c != r2) sum += fabs(a[c * N + r2]); a[r2 * N + r2] = sum; }
+    double* dA; long long* dc;
+    cudaMalloc(&dA, sizeof(double) * N * N); cudaMalloc(&dc, 8 * 4096);
+    cudaMemcpy(dA, a.data(), sizeof(double) * N * N, cudaMemcpyHostToDevice);
+    const int smem = (116 * 101 + 1600 + 640 + 64 + 8 * 1024) * 8;
+    cudaFuncSetAttribute(lab_prod, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int s0 : {0, 96, 108})
+      for (int nz : {0x00, 0xe3}) {
+        cudaMemset(dc, 0, 8 * 4096);
+        lab_prod<<<1, nz ? 256 : 32, smem>>>(dA, dc, 2000, s0, nz);
+        cudaError_t e = cudaDeviceSynchronize();
+        long long h[3]; cudaMemcpy(h, dc, 24, cudaMemcpyDeviceToHost);
+        printf("production potrf_diag on the ring: s0=%3d noise=%02x  %lld cycles/potrf (+ %lld refill)  fail-sum %lld (%s)\n",
+               s0, nz, h[0], h[1], h[2], cudaGetErrorString(e));
+      }
+    cudaFree(dA); cudaFree(dc);
+  }
   const int masks[] = {0x00, 0xe1, 0x11, 0x14, 0xe2, 0xe3, 0xf3};
   for (int m : masks) run<0>("v0 production", m);
   for (int m : masks) run<1>("v2 three-row lookahead", m);
