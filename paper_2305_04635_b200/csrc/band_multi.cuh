@@ -188,6 +188,27 @@ __device__ __forceinline__ void load_tile(double* s, const double* ab, const Mul
   }
 }
 
+// one tile whose upper triangle is don't-care: unmasked whenever the addresses are in bounds
+template <int NB, int NT>
+__device__ __forceinline__ void load_tile_unmasked_ok(double* s, const double* ab, const MultiGeom& g, int R, int C,
+                                                      int t) {
+  constexpr int LD = MultiTile<NB>::LD;
+  if (tile_loadable_unmasked(g, NB, R, C)) {
+    constexpr int CS = NT / NB, E = NB * NB / NT;
+    const int r = t % NB, c0 = t / NB;
+    const double* p = ab + (int64_t)(C * NB + c0) * g.ldab + ((R - C) * NB + r - c0);
+    const int64_t step = (int64_t)CS * (g.ldab - 1);
+    double v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = __ldcg(p + e * step);
+    double* q = s + c0 * LD + r;
+#pragma unroll
+    for (int e = 0; e < E; ++e) q[e * CS * LD] = v[e];
+  } else {
+    load_tile<NB, NT>(s, ab, g, R, C, t);
+  }
+}
+
 // tiles (R, C0) -> s0, (R, C1) -> s1 and, with K3, (R, C2) -> s2 in ONE L2 round trip
 template <int NB, int NT, bool K3>
 __device__ __forceinline__ void load_tiles3(double* s0, double* s1, double* s2, const double* ab, const MultiGeom& g,
@@ -479,7 +500,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
     // SYRK of (j+1,j+1); warps 4-7 write back and publish L(j,j), its inverse and L(j+1,j)
     // beside them.  On the chain per step: POTRF, two 32^3 tile products, three barriers.
     __shared__ __align__(8) unsigned long long colbar[8];
-    __shared__ int s_okx;
+    __shared__ int s_okx, s_okd;
     double* sD = smem;             // current diagonal tile (fully updated)
     double* sLp = smem + E;        // L(j, j-1) from the previous step
     double* sInv2 = smem + 2 * E;  // L(j,j)^-1 by step parity (sInv[k*LD + c] = Linv(c, k)): the
@@ -498,6 +519,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       s_fail = -1;
       s_ok = 1;
       s_okx = 1;
+      s_okd = 1;
       for (int i = 0; i < 8; ++i) mbar_init(colbar + i, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -534,17 +556,23 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
           // L(j,j-2), this CTA's own TRSM of the step before last, so it is applied here and
           // not behind a release -> worker -> release round trip
           const int need1 = has_v ? max(0, j - 2 - lo) : need;
-          if (t == 0) {
-            bool ok = spin_ge(TC(j + 1, 1), need1, ws.ctrl + 1, 64);
-            ok = ok && spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
-            if (has_v) ok = ok && spin_ge(LR(j + 1, 3), 1, ws.ctrl + 1, 64);
-            trace_stamp_to(tr, j, 6);
-            s_ok = ok;
+          // A(j+1,j) and L(j+1,j-2): their flags are a step old.  The diagonal tile A(j+1,j+1)
+          // is fetched by warp 5 (below): its last worker update is released ~2 K cycles into
+          // this step, and only the second lookback product needs it.
+          if (warp == 2) {
+            bool ok = true;
+            if (t == 0) ok = spin_ge(TC(j + 1, 1), need1, ws.ctrl + 1, 64);
+            if (t == 1 && has_v) ok = spin_ge(LR(j + 1, 3), 1, ws.ctrl + 1, 64);
+            ok = __all_sync(kFull, ok);
+            if (t == 0) {
+              trace_stamp_to(tr, j, 6);
+              s_ok = ok;
+            }
           }
           named_sync(6, 64);
           if (warp_uniform(s_ok)) {
-            if (has_v) load_tiles3<NB, 64, true>(sP, sD2, sV, ab, g, j + 1, j, j + 1, j - 2, t);
-            else load_tiles3<NB, 64, false>(sP, sD2, nullptr, ab, g, j + 1, j, j + 1, j - 2, t);
+            if (has_v) load_tiles3<NB, 64, false>(sP, sV, nullptr, ab, g, j + 1, j, j - 2, 0, t);
+            else load_tile<NB, 64>(sP, ab, g, j + 1, j, t);
           }
           if (t == 0) trace_stamp_to(tr, j, 7);  // (tiles loaded)
         }
@@ -553,17 +581,29 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         if (threadIdx.x == 64) trace_stamp_to(tr, j, 3);   // (lookback products start)
         if (has_w && warp_uniform(s_ok)) {
           // three products, each on all four warps (two per SM sub-partition 2 / 3: the FP64
-          // pipes of sub-partitions 0 / 1 stay with the POTRF and inverse chains)
+          // pipes of sub-partitions 0 / 1 stay with the POTRF and inverse chains); the one on
+          // the diagonal tile last: it waits for warp 5's load
           const int w4 = warp < 4 ? warp - 2 : warp - 4;
           tile_gemm<NB, true, 4>(sP, sW, sLp, w4, 5, 128);              // A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T
-          tile_gemm<NB, true, 4>(sD2, sW, sW, w4, 5, 128);              // A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
           if (has_v) tile_gemm<NB, true, 4>(sP, sV, sW2, w4, 5, 128);   // A(j+1,j)   -= L(j+1,j-2) L(j,j-2)^T
+          named_sync(10, 160);
+          if (warp_uniform(s_okd)) tile_gemm<NB, true, 4>(sD2, sW, sW, w4, 5, 128);  // A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
+        } else {
+          named_sync(10, 160);
         }
+      } else if (next && warp == 5) {
+        // (after this warp's write-back of L(j,j-1), above)
+        const int t = threadIdx.x - 160;
+        const int need = max(0, j - 1 - max(0, j + 1 - T));  // worker updates m in [lo, j-2]
+        if (t == 0) s_okd = spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
+        __syncwarp();
+        if (warp_uniform(s_okd)) load_tile_unmasked_ok<NB, 32>(sD2, ab, g, j + 1, j + 1, t);
+        named_sync(10, 160);
       }
       __syncthreads();
       if (threadIdx.x == 0) trace_stamp_to(tr, j, 2);
       const int fl = warp_uniform(s_fail);
-      const int okn = warp_uniform(s_ok) && warp_uniform(s_okx);
+      const int okn = warp_uniform(s_ok) && warp_uniform(s_okx) && warp_uniform(s_okd);
       if (fl >= 0) {
         fail_col = j * NB + fl;
         if (threadIdx.x == 0) atomicExch(ws.ctrl + 1, fail_col + 1);
