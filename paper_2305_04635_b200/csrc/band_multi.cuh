@@ -280,7 +280,8 @@ __device__ __forceinline__ void dmma884p(double& d0, double& d1, double a, doubl
 }
 template <int NB, bool kSub, int NW = 8, bool kBTri = false>
 __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const double* sB, int wg = threadIdx.x >> 5,
-                                          int bar_id = 0, int bar_cnt = kMultiThreads) {
+                                          int bar_id = 0, int bar_cnt = kMultiThreads, const double* sA2 = nullptr,
+                                          const double* sB2 = nullptr) {
   constexpr int LD = MultiTile<NB>::LD;
   constexpr int MT = NB / 8;
   constexpr int WM = (NB == 64) ? 2 : (NW < 4 ? NW : 4);  // warps along m
@@ -321,6 +322,24 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
         dmma884p(acc[tm][tn][0], acc[tm][tn][1], a[tm], b[tn]);
       }
   }
+  // optional second product into the same accumulators (C -= A B^T + A2 B2^T: one pass over C)
+  if (sA2) {
+#pragma unroll
+    for (int k0 = 0; k0 < NB; k0 += 4) {
+      double a[TM], b[TN];
+#pragma unroll
+      for (int tm = 0; tm < TM; ++tm) {
+        const double v = sA2[(k0 + gc) * LD + (wm * TM + tm) * 8 + gr];
+        a[tm] = kSub ? -v : v;
+      }
+#pragma unroll
+      for (int tn = 0; tn < TN; ++tn) b[tn] = sB2[(k0 + gc) * LD + (wn * TN + tn) * 8 + pb];
+#pragma unroll
+      for (int tm = 0; tm < TM; ++tm)
+#pragma unroll
+        for (int tn = 0; tn < TN; ++tn) dmma884p(acc[tm][tn][0], acc[tm][tn][1], a[tm], b[tn]);
+    }
+  }
   named_sync(bar_id, bar_cnt);  // sC may be read by other warps' fragment loads above (kSub)
 #pragma unroll
   for (int tm = 0; tm < TM; ++tm)
@@ -329,6 +348,45 @@ __device__ __forceinline__ void tile_gemm(double* sC, const double* sA, const do
       const int m = (wm * TM + tm) * 8 + gr, n0 = (wn * TN + tn) * 8;
       sC[(n0 + pc0) * LD + m] = acc[tm][tn][0];
       sC[(n0 + pc1) * LD + m] = acc[tm][tn][1];
+    }
+  named_sync(bar_id, bar_cnt);
+}
+
+// C -= A A^T on the LOWER 8x8 blocks of a 32x32 tile only (10 of 16: the upper triangle of a
+// diagonal tile is don't-care everywhere), four warps, blocks dealt 3/3/2/2.  Same fragment
+// conventions and kperm column order as tile_gemm.
+template <int NB>
+__device__ __forceinline__ void tile_syrk_lower4(double* sC, const double* sA, int w4, int bar_id, int bar_cnt) {
+  static_assert(NB == 32, "block lists below are for a 4x4 grid of 8x8 blocks");
+  constexpr int LD = MultiTile<NB>::LD;
+  // (tm, tn) per warp, packed 4 bits each; count in cnt
+  const unsigned tmv = w4 == 0 ? 0x033u : w4 == 1 ? 0x133u : w4 == 2 ? 0x22u : 0x12u;
+  const unsigned tnv = w4 == 0 ? 0x010u : w4 == 1 ? 0x032u : w4 == 2 ? 0x10u : 0x12u;
+  const int cnt = w4 < 2 ? 3 : 2;
+  const int lane = threadIdx.x & 31, gr = lane >> 2, gc = lane & 3;
+  const int pb = kperm(gr), pc0 = kperm(2 * gc), pc1 = kperm(2 * gc + 1);
+  double acc[3][2];
+  int mo[3], no[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    mo[b] = 8 * (int)((tmv >> (4 * b)) & 15u);
+    no[b] = 8 * (int)((tnv >> (4 * b)) & 15u);
+    acc[b][0] = b < cnt ? sC[(no[b] + pc0) * LD + mo[b] + gr] : 0.0;
+    acc[b][1] = b < cnt ? sC[(no[b] + pc1) * LD + mo[b] + gr] : 0.0;
+  }
+#pragma unroll
+  for (int k0 = 0; k0 < NB; k0 += 4) {
+    const double* col = sA + (k0 + gc) * LD;
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      if (b < cnt) dmma884p(acc[b][0], acc[b][1], -col[mo[b] + gr], col[no[b] + pb]);
+  }
+  named_sync(bar_id, bar_cnt);
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+    if (b < cnt) {
+      sC[(no[b] + pc0) * LD + mo[b] + gr] = acc[b][0];
+      sC[(no[b] + pc1) * LD + mo[b] + gr] = acc[b][1];
     }
   named_sync(bar_id, bar_cnt);
 }
@@ -558,7 +616,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
           const int need1 = has_v ? max(0, j - 2 - lo) : need;
           // A(j+1,j) and L(j+1,j-2): their flags are a step old.  The diagonal tile A(j+1,j+1)
           // is fetched by warp 5 (below): its last worker update is released ~2 K cycles into
-          // this step, and only the second lookback product needs it.
+          // this step, and only the last lookback product needs it.
           if (warp == 2) {
             bool ok = true;
             if (t == 0) ok = spin_ge(TC(j + 1, 1), need1, ws.ctrl + 1, 64);
@@ -576,18 +634,16 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
           }
           if (t == 0) trace_stamp_to(tr, j, 7);  // (tiles loaded)
         }
-        if (threadIdx.x == 192) trace_stamp_to(tr, j, 5);  // (warps 6-7 arrive: their TRSM is done)
         named_sync(5, 128);  // warps 2, 3, 6, 7: the tiles are in shared memory (sW is the pivot's own)
-        if (threadIdx.x == 64) trace_stamp_to(tr, j, 3);   // (lookback products start)
         if (has_w && warp_uniform(s_ok)) {
-          // three products, each on all four warps (two per SM sub-partition 2 / 3: the FP64
-          // pipes of sub-partitions 0 / 1 stay with the POTRF and inverse chains); the one on
-          // the diagonal tile last: it waits for warp 5's load
+          // A(j+1,j) -= L(j+1,j-1) L(j,j-1)^T + L(j+1,j-2) L(j,j-2)^T, one pass over the tile, on
+          // four warps (two per SM sub-partition 2 / 3: the FP64 pipes of sub-partitions 0 / 1
+          // stay with the POTRF and inverse chains)
           const int w4 = warp < 4 ? warp - 2 : warp - 4;
-          tile_gemm<NB, true, 4>(sP, sW, sLp, w4, 5, 128);              // A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T
-          if (has_v) tile_gemm<NB, true, 4>(sP, sV, sW2, w4, 5, 128);   // A(j+1,j)   -= L(j+1,j-2) L(j,j-2)^T
+          tile_gemm<NB, true, 4>(sP, sW, sLp, w4, 5, 128, has_v ? sV : nullptr, sW2);
+          // then the diagonal tile, once warp 5 has it: A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
           named_sync(10, 160);
-          if (warp_uniform(s_okd)) tile_gemm<NB, true, 4>(sD2, sW, sW, w4, 5, 128);  // A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T
+          if (warp_uniform(s_okd)) tile_syrk_lower4<NB>(sD2, sW, w4, 5, 128);
         } else {
           named_sync(10, 160);
         }
@@ -595,9 +651,14 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
         // (after this warp's write-back of L(j,j-1), above)
         const int t = threadIdx.x - 160;
         const int need = max(0, j - 1 - max(0, j + 1 - T));  // worker updates m in [lo, j-2]
-        if (t == 0) s_okd = spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
+        if (t == 0) {
+          trace_stamp_to(tr, j, 5);  // (warp 5 free for the diagonal tile)
+          s_okd = spin_ge(TC(j + 1, 0), need, ws.ctrl + 1, 64);
+          trace_stamp_to(tr, j, 4);  // (its flag seen)
+        }
         __syncwarp();
         if (warp_uniform(s_okd)) load_tile_unmasked_ok<NB, 32>(sD2, ab, g, j + 1, j + 1, t);
+        if (t == 0) trace_stamp_to(tr, j, 3);  // (diagonal tile loaded)
         named_sync(10, 160);
       }
       __syncthreads();
@@ -654,8 +715,7 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
       } else if (next) {
         tile_gemm<NB, false, 4, true>(sX, sP, sInv, warp, 2, 128);  // L(j+1,j) = A(j+1,j) L(j,j)^-T
         asm volatile("bar.arrive 4, 160;" ::: "memory");
-        tile_gemm<NB, true, 4>(sD2, sX, sX, warp, 2, 128);  // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T
-        if (threadIdx.x == 0) trace_stamp_to(tr, j, 4);
+        tile_syrk_lower4<NB>(sD2, sX, warp, 2, 128);  // A(j+1,j+1) -= L(j+1,j) L(j+1,j)^T (lower blocks)
       }
       if (!next) break;
       // rotate (every thread for itself, no barrier).  Buffers that lagging warps may still

@@ -150,8 +150,8 @@ def trace(tag):
     rel = lambda k: float(np.median(st[2:-2, k] - st[2:-2, 0]))  # noqa: E731
     out = {"config": tag, "steps": steps, "unit": "cycles", "total_cycles": float(st[-1, 1] - st[0, 0]),
            "step": float(np.median(np.diff(st[:, 0]))), "potrf_done": rel(1), "stage_barrier": rel(2),
-           "trsm_syrk_done": rel(4), "tiles_loaded": rel(7), "flags_seen": rel(6), "x2_prev_done": rel(5),
-           "lookback_start": rel(3)}
+           "tiles_loaded": rel(7), "flags_seen": rel(6), "diag_warp_free": rel(5), "diag_flag_seen": rel(4),
+           "diag_loaded": rel(3)}
     if t[-2] > 0:
         out["row_task_cycles"] = float(t[-3]) / float(t[-2])
     nb = (n + 31) // 32
