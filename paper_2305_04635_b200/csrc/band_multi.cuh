@@ -5,21 +5,27 @@
 // becomes in-kernel dataflow over NB x NB tiles of the band (tile (R, C) covers
 // rows R*NB.., columns C*NB..; T = ceil(kd/NB) sub-diagonal tiles per column):
 //
-//   * CTA 0 is the PIVOT.  Step j: warp 0 factors tile (j,j) with the warp-level
-//     redundant-chain POTRF while warps 1-7 wait for and load the tiles of the next
-//     step; then the critical near-diagonal work: tile (j+1,j) gets its last update
-//     (with L(j+1,j-1), L(j,j-1)) and its TRSM, tile (j+1,j+1) its last two updates
-//     -- so the chain POTRF(j) -> POTRF(j+1) never leaves the SM.  The pivot owns the
-//     updates (m+1,m+1,m), (m+2,m+1,m), (m+2,m+2,m).
-//   * CTAs 1.. are WORKERS pulling tasks in a fixed topological order from an
-//     atomic ticket: per step j the TRSMs L(R,j) = A(R,j) L(j,j)^-T for
-//     R = j+2..j+T, then the tile updates A(R,S) -= L(R,j) L(S,j)^T (R-major).
+//   * CTA 0 is the PIVOT: the whole near-diagonal chain stays in its shared memory.  Step j,
+//     stage A: warp 0 factors tile (j,j) (warp-level redundant-chain POTRF), warp 1 forms
+//     L(j,j)^-1 in lock step, the others fetch A(j+1,j), A(j+1,j+1) and L(j+1,j-2) and apply
+//     the lookback products (with L(j+1,j-1), the pivot's own TRSM of the step before, and
+//     L(j,j-1), L(j,j-2)); stage B: L(j+1,j) and L(j+2,j) as products with L(j,j)^-1, SYRK of
+//     (j+1,j+1), and straight into the next POTRF; write-backs and flag releases run behind,
+//     asynchronously.  One CTA barrier per step.  The pivot owns the TRSMs of rows j+1, j+2
+//     and the updates (m+1,m+1,m), (m+2,m+1,m), (m+2,m+2,m), (m+3,m+2,m).
+//   * CTAs 1.. are WORKERS pulling tasks in a fixed topological order from an atomic
+//     ticket.  Per super-step s: (A) step s-1's updates of tile column s+1, (B) the ROW OWNER
+//     of the row entering the band -- one group runs the row's whole chain TRSM L(R,m) ->
+//     update of (R,m+1) -> TRSM L(R,m+1) ... for m = R-T .. R-3, the tile staying in shared
+//     memory between links -- (C) step s-1's other tile updates A(R,S) -= L(R,m) L(S,m)^T.
 //     A task spins (ld.acquire.gpu + nanosleep) on per-tile flags:
 //       lrdy[R][d]  L(R, R-d) final and published,
 //       tcnt[R][d]  number of worker updates applied to tile (R, R-d).
 //     Tickets are handed out in dependency order and every CTA is co-resident
 //     (cooperative launch), so every wait is on work already owned by a running
-//     CTA: no deadlock.  A failing pivot sets `fail`, which every spin polls.
+//     CTA: no deadlock (a row owner holds its group for up to T steps, so row owners are
+//     used only when the grid has >= 2T+16 groups).  A failing pivot sets `fail`, which
+//     every spin polls.
 //
 // Tile GEMMs use the FP64 tensor path (mma.sync m8n8k4 f64 -> DMMA.8x8x4);
 // tiles are staged in shared memory column-major with a padded leading
@@ -551,12 +557,13 @@ band_multi_kernel(double* __restrict__ ab, MultiGeom g, MultiWs ws, int32_t* inf
     // Warp roles (warp w sits on SM sub-partition w & 3):
     //   0      POTRF of (j,j)                       -- the chain, alone on SMSP 0 in stage A
     //   1      L(j,j)^-1 in lock step behind it
-    //   2,3    lookback A(j+1,j)   -= L(j+1,j-1) L(j,j-1)^T     } stage A, as soon as the
-    //   6,7    lookback A(j+1,j+1) -= L(j+1,j-1) L(j+1,j-1)^T   } tiles have landed
-    //   4-7    service: flag waits, tile loads, write-backs and publishes
+    //   2,3    flags + loads of A(j+1,j), L(j+1,j-2)
+    //   2,3,6,7  the lookback products (DMMA on SMSPs 2-3 only)
+    //   4,5    service, no FP64: write-backs and flag releases of the previous stage B, the
+    //          late flag + load of the diagonal tile A(j+1,j+1) (warp 5)
     // Stage B (after the POTRF): warps 0-3 run the TRSM as a product with L(j,j)^-1 and the
-    // SYRK of (j+1,j+1); warps 4-7 write back and publish L(j,j), its inverse and L(j+1,j)
-    // beside them.  On the chain per step: POTRF, two 32^3 tile products, three barriers.
+    // SYRK of (j+1,j+1) and go on to the next POTRF; warps 6-7 form L(j+2,j); warps 4-5 write
+    // back and publish L(j,j)^-1, L(j,j), L(j+1,j), L(j+2,j) behind them.
     __shared__ __align__(8) unsigned long long colbar[8];
     __shared__ int s_okx, s_okd;
     double* sD = smem;             // current diagonal tile (fully updated)
